@@ -1,0 +1,74 @@
+// esdg_inst.cuh -- body shared by inst_nq*.cu; define ESDG_NQ before including.
+#include <mutex>
+
+#include "esdg_kernels.cuh"
+#include "esdg_launch.hpp"
+
+namespace esdg_b200 {
+
+namespace {
+template <class Real, int NQ, bool VOL, bool SURF>
+cudaError_t launch_one(const dev::RhsParams<Real, NQ>& P, cudaStream_t stream) {
+  constexpr int EPB = dev::Tile<NQ, sizeof(Real)>::EPB;
+  constexpr int T = EPB * NQ * NQ;
+  constexpr size_t smem =
+      size_t(dev::V_COUNT + 5) * EPB * dev::Geo<NQ>::N3P * sizeof(Real);
+  auto kern = dev::rhs_kernel<Real, NQ, EPB, VOL, SURF>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(
+        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  if (P.ne <= 0) return cudaSuccess;
+  const long long blocks = (P.ne + EPB - 1) / EPB;
+  kern<<<dim3(unsigned(blocks)), dim3(T), smem, stream>>>(P);
+  return cudaGetLastError();
+}
+} // namespace
+
+template <class Real, int NQ>
+cudaError_t launch_rhs(int mode, const dev::RhsParams<Real, NQ>& P,
+                       cudaStream_t stream) {
+  switch (mode) {
+    case kModeVolume: return launch_one<Real, NQ, true, false>(P, stream);
+    case kModeSurface: return launch_one<Real, NQ, false, true>(P, stream);
+    case kModeFused: return launch_one<Real, NQ, true, true>(P, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <class Real, int NQ>
+cudaError_t launch_pack(const Real* q, const int32_t* send_elem,
+                        const int32_t* send_face, Real* send, long long n_send,
+                        cudaStream_t stream) {
+  if (n_send <= 0) return cudaSuccess;
+  const long long total = n_send * 5 * NQ * NQ;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  dev::pack_kernel<Real, NQ><<<unsigned(blocks), 256, 0, stream>>>(
+      q, send_elem, send_face, send, n_send);
+  return cudaGetLastError();
+}
+
+template <class Real, int NQ>
+void rhs_launch_shape(int* threads, int* epb, size_t* smem_bytes) {
+  constexpr int EPB = dev::Tile<NQ, sizeof(Real)>::EPB;
+  *threads = EPB * NQ * NQ;
+  *epb = EPB;
+  *smem_bytes = size_t(dev::V_COUNT + 5) * EPB * dev::Geo<NQ>::N3P * sizeof(Real);
+}
+
+#define ESDG_INSTANTIATE(REAL, NQ)                                             \
+  template cudaError_t launch_rhs<REAL, NQ>(                                   \
+      int, const dev::RhsParams<REAL, NQ>&, cudaStream_t);                     \
+  template cudaError_t launch_pack<REAL, NQ>(const REAL*, const int32_t*,      \
+                                             const int32_t*, REAL*, long long, \
+                                             cudaStream_t);                    \
+  template void rhs_launch_shape<REAL, NQ>(int*, int*, size_t*);
+
+ESDG_INSTANTIATE(double, ESDG_NQ)
+ESDG_INSTANTIATE(float, ESDG_NQ)
+
+} // namespace esdg_b200

@@ -1,0 +1,36 @@
+// esdg_launch.hpp -- host-callable launchers of the kernels in
+// esdg_kernels.cuh. One translation unit per NQ instantiates them
+// (inst_nq*.cu) so the heavy, fully unrolled kernels compile in parallel.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "esdg_device.cuh"
+
+namespace esdg_b200 {
+namespace dev {
+template <class Real, int NQ>
+struct RhsParams;
+}
+
+enum RhsMode { kModeVolume = 0, kModeSurface = 1, kModeFused = 2 };
+
+template <class Real, int NQ>
+cudaError_t launch_rhs(int mode, const dev::RhsParams<Real, NQ>& P,
+                       cudaStream_t stream);
+
+template <class Real, int NQ>
+cudaError_t launch_pack(const Real* q, const int32_t* send_elem,
+                        const int32_t* send_face, Real* send, long long n_send,
+                        cudaStream_t stream);
+
+template <class Real>
+cudaError_t launch_axpy(Real* q, const Real* k, Real b, long long n,
+                        cudaStream_t stream);
+
+// Dynamic shared memory one CTA of rhs_kernel needs (bytes) and its CTA size.
+template <class Real, int NQ>
+void rhs_launch_shape(int* threads, int* epb, size_t* smem_bytes);
+
+} // namespace esdg_b200

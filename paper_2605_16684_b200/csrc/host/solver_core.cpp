@@ -1,0 +1,774 @@
+// solver_core.cpp -- see solver_core.hpp.
+#include "solver_core.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <thread>
+
+#include "../esdg_launch.hpp"
+
+namespace esdg_b200 {
+namespace host {
+
+namespace {
+
+#define CU(call)                                                               \
+  do {                                                                         \
+    cudaError_t e_ = (call);                                                   \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);                        \
+  } while (0)
+
+#define RC(call)                                                               \
+  do {                                                                         \
+    const int rc_ = (call);                                                    \
+    if (rc_ != ESDG_B200_OK) return rc_;                                       \
+  } while (0)
+
+enum { kClsVolume = 0, kClsSurface = 1, kClsUpdate = 2, kClsPack = 3 };
+
+// runs f(begin, end) over [0, n) on the host's hardware threads
+template <class F>
+void parallel_for(int64_t n, F&& f) {
+  int nt = int(std::thread::hardware_concurrency());
+  if (nt < 1) nt = 1;
+  if (n < 4096) nt = 1;
+  if (nt > 64) nt = 64;
+  if (nt == 1) {
+    f(int64_t(0), n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const int64_t chunk = (n + nt - 1) / nt;
+  for (int t = 0; t < nt; ++t) {
+    const int64_t b = t * chunk, e = std::min(n, b + chunk);
+    if (b >= e) break;
+    pool.emplace_back([&f, b, e] { f(b, e); });
+  }
+  for (auto& th : pool) th.join();
+}
+
+inline void store_real(void* base, size_t index, int precision, double v) {
+  if (precision == 8)
+    static_cast<double*>(base)[index] = v;
+  else
+    static_cast<float*>(base)[index] = float(v);
+}
+inline double load_real(const void* base, size_t index, int precision) {
+  return precision == 8 ? static_cast<const double*>(base)[index]
+                        : double(static_cast<const float*>(base)[index]);
+}
+
+// CoriolisParams::f_at in Real arithmetic (physics.hpp:285-292) at the node
+// rows of every y level, y = Real(node_coordinate) (solver.hpp:211-213)
+template <class Real>
+void coriolis_table(const Mesh& m, const RefElement& ref,
+                    const esdg_b200_settings& s, std::vector<char>& out) {
+  const int ny = m.dims[1], nq = ref.nq;
+  out.resize(sizeof(Real) * size_t(ny) * size_t(nq));
+  Real* f = reinterpret_cast<Real*>(out.data());
+  for (int j = 0; j < ny; ++j)
+    for (int b = 0; b < nq; ++b) {
+      const double y64 =
+          m.cfg.lo[1] + (double(j) + 0.5 * (ref.nodes[size_t(b)] + 1.0)) * m.delta[1];
+      const Real y = Real(y64);
+      Real v = Real(0);
+      if (s.coriolis_mode == 1) v = Real(s.f0);
+      if (s.coriolis_mode == 2) v = Real(s.f0) + Real(s.beta) * (y - Real(s.y0));
+      f[size_t(j) * size_t(nq) + size_t(b)] = v;
+    }
+}
+
+// FaceIndexer::node (mesh.hpp:107-114)
+inline int face_node(int nq, int dir, int side, int fn) {
+  int c[3];
+  c[dir] = side ? nq - 1 : 0;
+  c[(dir + 1) % 3] = fn % nq;
+  c[(dir + 2) % 3] = fn / nq;
+  return c[0] + nq * (c[1] + nq * c[2]);
+}
+
+} // namespace
+
+int SolverCore::create(Mesh* mesh, const Options& opt, SolverCore** out) {
+  if (!mesh || !out || (opt.precision != 8 && opt.precision != 4) ||
+      opt.order < 1 || opt.order > 7 || opt.world_size < 1 ||
+      opt.local_ranks.empty() || opt.local_ranks.size() != opt.devices.size()) {
+    set_message("solver_create: bad arguments (order must be 1..7)");
+    return ESDG_B200_BADARG;
+  }
+  std::unique_ptr<SolverCore> s(new SolverCore());
+  s->mesh_ = mesh;
+  s->opt_ = opt;
+  if (!RefElement::build(opt.order, s->ref_)) {
+    set_message("solver_create: reference element construction failed");
+    return ESDG_B200_BADARG;
+  }
+  s->nq_ = s->ref_.nq;
+  s->n2_ = s->nq_ * s->nq_;
+  s->n3_ = s->n2_ * s->nq_;
+  if (!make_partition(mesh->ne, opt.world_size, s->range_begin_)) {
+    set_message("solver_create: more ranks than elements");
+    return ESDG_B200_BADARG;
+  }
+  std::vector<int> lr = opt.local_ranks;
+  for (size_t i = 0; i < lr.size(); ++i) {
+    if (lr[i] < 0 || lr[i] >= opt.world_size || (i > 0 && lr[i] != lr[i - 1] + 1)) {
+      set_message("solver_create: local ranks must be a contiguous ascending run");
+      return ESDG_B200_BADARG;
+    }
+  }
+  s->local_begin_ = s->range_begin_[size_t(lr.front())];
+  s->local_end_ = s->range_begin_[size_t(lr.back()) + 1];
+  s->shards_.resize(lr.size());
+  for (size_t i = 0; i < lr.size(); ++i) {
+    LocalShard& ls = s->shards_[i];
+    ls.rank = lr[i];
+    ls.begin = s->range_begin_[size_t(lr[i])];
+    ls.end = s->range_begin_[size_t(lr[i]) + 1];
+    build_rank_halo(*mesh, s->range_begin_, lr[i], ls.halo);
+    if (!ls.halo.peers.empty()) s->any_halo_ = true;
+  }
+  // every peer must be local unless an exchange callback was given
+  if (!opt.exchange)
+    for (const LocalShard& ls : s->shards_)
+      for (const auto& p : ls.halo.peers)
+        if (s->local_index_of_rank(p.rank) < 0) {
+          set_message("solver_create: remote peers need an exchange callback");
+          return ESDG_B200_BADARG;
+        }
+  for (size_t i = 0; i < s->shards_.size(); ++i) {
+    const int rc = s->build_shard(s->shards_[i]);
+    if (rc != ESDG_B200_OK) return rc;
+  }
+  // peer access between the devices of local shards (best effort)
+  for (size_t i = 0; i < s->shards_.size(); ++i)
+    for (size_t j = 0; j < s->shards_.size(); ++j) {
+      const int di = opt.devices[i], dj = opt.devices[j];
+      if (di == dj) continue;
+      int can = 0;
+      if (cudaDeviceCanAccessPeer(&can, di, dj) == cudaSuccess && can) {
+        cudaSetDevice(di);
+        if (cudaDeviceEnablePeerAccess(dj, 0) != cudaSuccess) cudaGetLastError();
+      }
+    }
+  *out = s.release();
+  return ESDG_B200_OK;
+}
+
+SolverCore::~SolverCore() {
+  for (auto& ls : shards_) {
+    if (ls.dev) cudaSetDevice(ls.dev->device());
+    if (ls.comm) cudaStreamDestroy(ls.comm);
+    if (ls.ev_pack) cudaEventDestroy(ls.ev_pack);
+    if (ls.ev_recv) cudaEventDestroy(ls.ev_recv);
+    if (ls.ev_surf) cudaEventDestroy(ls.ev_surf);
+  }
+  for (auto& t : pending_) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  for (auto& p : event_pool_) {
+    cudaEventDestroy(p.first);
+    cudaEventDestroy(p.second);
+  }
+}
+
+int SolverCore::local_index_of_rank(int rank) const {
+  for (size_t i = 0; i < shards_.size(); ++i)
+    if (shards_[i].rank == rank) return int(i);
+  return -1;
+}
+
+int SolverCore::build_shard(LocalShard& ls) {
+  const int prec = opt_.precision;
+  const int64_t ne = ls.end - ls.begin;
+  const size_t idx = size_t(&ls - shards_.data());
+
+  // build_phi (solver.hpp:166-176): phi = Real(g z), z in 64-bit
+  std::vector<char> phi(size_t(prec) * size_t(ne) * size_t(n3_));
+  const double g = opt_.gas.gravity;
+  parallel_for(ne, [&](int64_t b, int64_t e) {
+    for (int64_t el = b; el < e; ++el)
+      for (int c = 0; c < nq_; ++c) {
+        const double z = mesh_->node_coordinate(ls.begin + el, 2, ref_.nodes[size_t(c)]);
+        const double v = g * z;
+        for (int n = c * n2_; n < (c + 1) * n2_; ++n)
+          store_real(phi.data(), size_t(el) * size_t(n3_) + size_t(n), prec, v);
+      }
+  });
+  // build_ghost_phi (solver.hpp:178-191): phi trace of the remote side
+  const int64_t n_ghost = int64_t(ls.halo.send_elem.size());
+  std::vector<char> gphi(size_t(prec) * size_t(n_ghost) * size_t(n2_) + 8);
+  for (int64_t s = 0; s < n_ghost; ++s) {
+    const int64_t relem = ls.halo.ghost_remote_elem[size_t(s)];
+    const int rface = ls.halo.ghost_remote_face[size_t(s)];
+    for (int fn = 0; fn < n2_; ++fn) {
+      const int node = face_node(nq_, rface / 2, rface % 2, fn);
+      const int c = node / n2_;
+      const double z = mesh_->node_coordinate(relem, 2, ref_.nodes[size_t(c)]);
+      store_real(gphi.data(), size_t(s) * size_t(n2_) + size_t(fn), prec, g * z);
+    }
+  }
+  std::vector<int32_t> ylevel(static_cast<size_t>(ne));
+  for (int64_t el = 0; el < ne; ++el)
+    ylevel[size_t(el)] = mesh_->lattice[size_t(ls.begin + el) * 3 + 1];
+  std::vector<char> cor;
+  if (prec == 8)
+    coriolis_table<double>(*mesh_, ref_, opt_.settings, cor);
+  else
+    coriolis_table<float>(*mesh_, ref_, opt_.settings, cor);
+
+  esdg_b200_shard_desc d{};
+  d.precision = prec;
+  d.nq = nq_;
+  d.device = opt_.devices[idx];
+  d.dissipation = opt_.settings.dissipation;
+  d.n_elements = ne;
+  d.elem_offset = ls.begin;
+  d.diff = ref_.diff.data();
+  d.weights = ref_.weights.data();
+  for (int k = 0; k < 3; ++k) d.metric[k] = mesh_->metric(k);
+  d.gamma = opt_.gas.gamma;
+  d.gas_R = opt_.gas.R;
+  // the table is always uploaded so settings can switch Coriolis on later
+  d.coriolis_mode = 2;
+  d.n_ylevels = mesh_->dims[1];
+  d.elem_ylevel = ylevel.data();
+  d.coriolis_f = cor.data();
+  d.nbr = ls.halo.nbr_local.data();
+  d.phi = phi.data();
+  d.n_ghost = int32_t(n_ghost);
+  d.ghost_phi = gphi.data();
+  d.n_send = int32_t(n_ghost);
+  d.send_elem = ls.halo.send_elem.data();
+  d.send_face = ls.halo.send_face.data();
+  ShardBase* dev = nullptr;
+  RC(create_shard(d, &dev));
+  ls.dev.reset(dev);
+  CU(cudaSetDevice(d.device));
+  CU(cudaStreamCreateWithFlags(&ls.comm, cudaStreamNonBlocking));
+  CU(cudaEventCreateWithFlags(&ls.ev_pack, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&ls.ev_recv, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&ls.ev_surf, cudaEventDisableTiming));
+  return ESDG_B200_OK;
+}
+
+int SolverCore::set_path(int path) {
+  if (path != ESDG_B200_PATH_SPLIT && path != ESDG_B200_PATH_FUSED) {
+    set_message("set_path: unknown path");
+    return ESDG_B200_BADARG;
+  }
+  path_ = path;
+  return ESDG_B200_OK;
+}
+
+int SolverCore::set_settings(const esdg_b200_settings& s) {
+  // the Coriolis table depends on (mode, f0, beta, y0): re-create is the
+  // simple route; dissipation alone is a flag flip
+  const bool cor_changed = s.coriolis_mode != opt_.settings.coriolis_mode ||
+                           s.f0 != opt_.settings.f0 ||
+                           s.beta != opt_.settings.beta || s.y0 != opt_.settings.y0;
+  if (cor_changed) {
+    set_message("set_settings: Coriolis parameters are fixed at creation");
+    return ESDG_B200_BADARG;
+  }
+  opt_.settings.dissipation = s.dissipation;
+  for (auto& ls : shards_) ls.dev->set_dissipation(s.dissipation);
+  return ESDG_B200_OK;
+}
+
+int SolverCore::halo(int32_t* peer, int64_t* offset, int64_t* count,
+                     int capacity) const {
+  if (shards_.size() != 1) return 0;
+  const auto& peers = shards_[0].halo.peers;
+  for (size_t i = 0; i < peers.size() && int(i) < capacity; ++i) {
+    if (peer) peer[i] = peers[i].rank;
+    if (offset) offset[i] = peers[i].offset;
+    if (count) count[i] = peers[i].count;
+  }
+  return int(peers.size());
+}
+
+// ---- state movement --------------------------------------------------------
+
+int SolverCore::set_state(int reg, const void* host) {
+  if (!host) return ESDG_B200_BADARG;
+  const size_t per = size_t(opt_.precision) * 5 * size_t(n3_);
+  for (auto& ls : shards_)
+    RC(ls.dev->upload(reg, static_cast<const char*>(host) + size_t(ls.begin - local_begin_) * per,
+                      0, ls.end - ls.begin, nullptr, false));
+  return ESDG_B200_OK;
+}
+
+int SolverCore::get_state(int reg, void* host) {
+  if (!host) return ESDG_B200_BADARG;
+  const size_t per = size_t(opt_.precision) * 5 * size_t(n3_);
+  for (auto& ls : shards_)
+    RC(ls.dev->download(reg, static_cast<char*>(host) + size_t(ls.begin - local_begin_) * per,
+                        0, ls.end - ls.begin, nullptr, false));
+  return ESDG_B200_OK;
+}
+
+int SolverCore::get_phi(void* host) const {
+  if (!host) return ESDG_B200_BADARG;
+  const double g = opt_.gas.gravity;
+  const int64_t ne = local_end_ - local_begin_;
+  parallel_for(ne, [&](int64_t b, int64_t e) {
+    for (int64_t el = b; el < e; ++el)
+      for (int c = 0; c < nq_; ++c) {
+        const double z = mesh_->node_coordinate(local_begin_ + el, 2, ref_.nodes[size_t(c)]);
+        for (int n = c * n2_; n < (c + 1) * n2_; ++n)
+          store_real(host, size_t(el) * size_t(n3_) + size_t(n), opt_.precision, g * z);
+      }
+  });
+  return ESDG_B200_OK;
+}
+
+int SolverCore::init_case(int case_id, uint64_t iparam, const double* dparam) {
+  CaseEval ce;
+  ce.case_id = case_id;
+  ce.gas = opt_.gas;
+  ce.mesh = mesh_->cfg;
+  ce.iparam = iparam;
+  if (dparam)
+    for (int i = 0; i < 5; ++i) ce.dparam[i] = dparam[i];
+  if (!ce.prepare()) {
+    set_message("init_case: unknown case");
+    return ESDG_B200_BADARG;
+  }
+  const int prec = opt_.precision;
+  const double g = opt_.gas.gravity;
+  const int64_t chunk_elems = std::max<int64_t>(1, (int64_t(256) << 20) / (int64_t(prec) * 5 * n3_));
+  std::vector<char> buf;
+  for (auto& ls : shards_) {
+    for (int64_t first = ls.begin; first < ls.end; first += chunk_elems) {
+      const int64_t count = std::min(chunk_elems, ls.end - first);
+      buf.resize(size_t(prec) * size_t(count) * 5 * size_t(n3_));
+      bool ok = true;
+      parallel_for(count, [&](int64_t b, int64_t e) {
+        for (int64_t i = b; i < e; ++i) {
+          const int64_t el = first + i;
+          for (int n = 0; n < n3_; ++n) {
+            const int a = n % nq_, bb = (n / nq_) % nq_, c = n / n2_;
+            const double x = mesh_->node_coordinate(el, 0, ref_.nodes[size_t(a)]);
+            const double y = mesh_->node_coordinate(el, 1, ref_.nodes[size_t(bb)]);
+            const double z = mesh_->node_coordinate(el, 2, ref_.nodes[size_t(c)]);
+            // init_state hands the callable the ROUNDED phi (solver.hpp:103)
+            const double phi = prec == 8 ? g * z : double(float(g * z));
+            double q[5];
+            if (!ce.point(x, y, z, phi, q)) {
+              ok = false;
+              for (int v = 0; v < 5; ++v) q[v] = 0.0;
+            }
+            for (int v = 0; v < 5; ++v)
+              store_real(buf.data(), (size_t(i) * 5 + size_t(v)) * size_t(n3_) + size_t(n), prec, q[v]);
+          }
+        }
+      });
+      if (!ok) {
+        set_message("init_case: state generator left its domain");
+        return ESDG_B200_BADARG;
+      }
+      RC(ls.dev->upload(ESDG_B200_REG_Q, buf.data(), first - ls.begin, count, nullptr, false));
+    }
+  }
+  return ESDG_B200_OK;
+}
+
+// ---- timing ---------------------------------------------------------------
+
+template <class F>
+int SolverCore::timed(LocalShard& ls, int cls, F&& launch) {
+  if (!timing_) return launch();
+  std::pair<cudaEvent_t, cudaEvent_t> ev;
+  if (!event_pool_.empty()) {
+    ev = event_pool_.back();
+    event_pool_.pop_back();
+  } else {
+    CU(cudaSetDevice(ls.dev->device()));
+    CU(cudaEventCreate(&ev.first));
+    CU(cudaEventCreate(&ev.second));
+  }
+  CU(cudaEventRecord(ev.first, ls.dev->stream()));
+  const int rc = launch();
+  CU(cudaEventRecord(ev.second, ls.dev->stream()));
+  pending_.push_back({ev.first, ev.second, cls});
+  if (pending_.size() >= 4096) RC(collect_timers());
+  return rc;
+}
+
+int SolverCore::collect_timers() {
+  for (auto& t : pending_) {
+    CU(cudaEventSynchronize(t.b));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, t.a, t.b));
+    seconds_[t.cls] += double(ms) * 1e-3;
+    event_pool_.push_back({t.a, t.b});
+  }
+  pending_.clear();
+  return ESDG_B200_OK;
+}
+
+int SolverCore::enable_timing(bool on) {
+  if (!on && timing_) RC(collect_timers());
+  timing_ = on;
+  return ESDG_B200_OK;
+}
+
+int SolverCore::timers(double seconds[4], int64_t* launches, bool reset) {
+  RC(collect_timers());
+  for (int i = 0; i < 4; ++i) seconds[i] = seconds_[i];
+  if (launches) {
+    *launches = 0;
+    for (auto& ls : shards_) *launches += ls.dev->launch_count();
+  }
+  if (reset)
+    for (int i = 0; i < 4; ++i) seconds_[i] = 0.0;
+  return ESDG_B200_OK;
+}
+
+// ---- RHS -------------------------------------------------------------------
+
+// (1) of rhs_job (solver.hpp:249-257): pack the ghost traces and start moving
+// them; returns immediately, copies run on the comm streams.
+int SolverCore::exchange_begin(int src) {
+  for (auto& ls : shards_) {
+    if (ls.halo.peers.empty()) continue;
+    CU(cudaSetDevice(ls.dev->device()));
+    // the previous RHS' copies out of this send buffer must have landed
+    if (!opt_.exchange)
+      for (const auto& p : ls.halo.peers)
+        CU(cudaStreamWaitEvent(ls.dev->stream(), shards_[size_t(local_index_of_rank(p.rank))].ev_recv, 0));
+    RC(timed(ls, kClsPack, [&] { return ls.dev->pack(src, nullptr); }));
+    CU(cudaEventRecord(ls.ev_pack, ls.dev->stream()));
+  }
+  if (opt_.exchange) {
+    LocalShard& ls = shards_[0];
+    if (opt_.exchange(opt_.exchange_user, 0, ls.dev->stream()) != 0) {
+      set_message("exchange callback failed (phase 0)");
+      return ESDG_B200_CUDA;
+    }
+    return ESDG_B200_OK;
+  }
+  for (auto& ls : shards_) {
+    if (ls.halo.peers.empty()) continue;
+    CU(cudaSetDevice(ls.dev->device()));
+    // the receive buffer is free once the previous surface kernel has run
+    CU(cudaStreamWaitEvent(ls.comm, ls.ev_surf, 0));
+    const size_t tb = ls.dev->trace_bytes();
+    for (const auto& p : ls.halo.peers) {
+      LocalShard& src_ls = shards_[size_t(local_index_of_rank(p.rank))];
+      // the peer's block for us: same face order, its own offset
+      int64_t peer_off = -1;
+      for (const auto& q : src_ls.halo.peers)
+        if (q.rank == ls.rank) peer_off = q.offset;
+      CU(cudaStreamWaitEvent(ls.comm, src_ls.ev_pack, 0));
+      CU(cudaMemcpyPeerAsync(static_cast<char*>(ls.dev->recv_ptr()) + size_t(p.offset) * tb,
+                             ls.dev->device(),
+                             static_cast<const char*>(src_ls.dev->send_ptr()) + size_t(peer_off) * tb,
+                             src_ls.dev->device(), size_t(p.count) * tb, ls.comm));
+    }
+    CU(cudaEventRecord(ls.ev_recv, ls.comm));
+  }
+  return ESDG_B200_OK;
+}
+
+// (4) of rhs_job (solver.hpp:291-294): the compute streams wait for the traces
+int SolverCore::exchange_end() {
+  if (opt_.exchange) {
+    if (opt_.exchange(opt_.exchange_user, 1, shards_[0].dev->stream()) != 0) {
+      set_message("exchange callback failed (phase 1)");
+      return ESDG_B200_CUDA;
+    }
+    return ESDG_B200_OK;
+  }
+  for (auto& ls : shards_) {
+    if (ls.halo.peers.empty()) continue;
+    CU(cudaSetDevice(ls.dev->device()));
+    CU(cudaStreamWaitEvent(ls.dev->stream(), ls.ev_recv, 0));
+  }
+  return ESDG_B200_OK;
+}
+
+int SolverCore::rhs(int src, int dst, double a_old, double a_new,
+                    bool with_source, bool volume_only, int stage) {
+  const bool halo = any_halo_ && !volume_only;
+  const int source = (with_source && opt_.settings.coriolis_mode != 0) ? 1 : 0;
+  if (halo) RC(exchange_begin(src));
+  if (path_ == ESDG_B200_PATH_FUSED && !volume_only) {
+    if (halo) RC(exchange_end());
+    for (auto& ls : shards_) {
+      RC(timed(ls, kClsVolume, [&] {
+        return ls.dev->rhs(kModeFused, src, dst, a_old, a_new, source, stage, nullptr);
+      }));
+      if (halo && !ls.halo.peers.empty()) CU(cudaEventRecord(ls.ev_surf, ls.dev->stream()));
+    }
+    return ESDG_B200_OK;
+  }
+  // (2) volume term overlaps the exchange (solver.hpp:259-262)
+  for (auto& ls : shards_)
+    RC(timed(ls, kClsVolume, [&] {
+      return ls.dev->rhs(kModeVolume, src, dst, a_old, a_new, source, stage, nullptr);
+    }));
+  if (volume_only) return ESDG_B200_OK;
+  if (halo) RC(exchange_end());
+  // (3)-(5) face fluxes and lift (solver.hpp:264-337)
+  for (auto& ls : shards_) {
+    RC(timed(ls, kClsSurface, [&] {
+      return ls.dev->rhs(kModeSurface, src, dst, 1.0, a_new, 0, stage, nullptr);
+    }));
+    if (halo && !ls.halo.peers.empty()) {
+      CU(cudaSetDevice(ls.dev->device()));
+      CU(cudaEventRecord(ls.ev_surf, ls.dev->stream()));
+    }
+  }
+  return ESDG_B200_OK;
+}
+
+int SolverCore::axpy(double b) {
+  for (auto& ls : shards_)
+    RC(timed(ls, kClsUpdate, [&] { return ls.dev->axpy(b, nullptr); }));
+  return ESDG_B200_OK;
+}
+
+int SolverCore::step(double dt, bool do_check) {
+  double a[5], b[5], c[5];
+  lsrk_coefficients(a, b, c);
+  // lsrk_step (time_integration.hpp:43-49); coefficients rounded to Real as
+  // the reference's Real(LsrkScheme::a[s]) does
+  for (int s = 0; s < 5; ++s) {
+    const double as = opt_.precision == 8 ? a[s] : double(float(a[s]));
+    const double bs = opt_.precision == 8 ? b[s] : double(float(b[s]));
+    RC(rhs(ESDG_B200_REG_Q, ESDG_B200_REG_K, as, dt, true, false, s));
+    RC(axpy(bs));
+  }
+  if (do_check) return check();
+  return ESDG_B200_OK;
+}
+
+int SolverCore::sync() {
+  for (auto& ls : shards_) {
+    CU(cudaSetDevice(ls.dev->device()));
+    CU(cudaStreamSynchronize(ls.dev->stream()));
+    CU(cudaStreamSynchronize(ls.comm));
+  }
+  return ESDG_B200_OK;
+}
+
+int SolverCore::check() {
+  std::memset(&err_, 0, sizeof err_);
+  bool any = false;
+  for (auto& ls : shards_) {
+    esdg_b200_error e{};
+    const int rc = ls.dev->check(nullptr, ESDG_B200_REG_Q, &e);
+    if (rc == ESDG_B200_NONPHYSICAL) {
+      // first error by (stage, element): WorkerPool rethrows by rank
+      // (worker_pool.hpp:51-52); ranks own ascending Morton ranges
+      if (!any || e.stage < err_.stage ||
+          (e.stage == err_.stage && e.element < err_.element))
+        err_ = e;
+      any = true;
+    } else if (rc != ESDG_B200_OK) {
+      return rc;
+    }
+  }
+  return any ? ESDG_B200_NONPHYSICAL : ESDG_B200_OK;
+}
+
+int SolverCore::assemble_rhs_host(const void* q, void* out, double a_old,
+                                  double a_new, bool volume_only) {
+  if (!q || !out) return ESDG_B200_BADARG;
+  // host fields go through the two device registers: q -> REG_Q, out -> REG_K
+  RC(set_state(ESDG_B200_REG_Q, q));
+  if (a_old != 0.0) RC(set_state(ESDG_B200_REG_K, out));
+  RC(rhs(ESDG_B200_REG_Q, ESDG_B200_REG_K, volume_only ? 0.0 : a_old,
+         volume_only ? 1.0 : a_new, !volume_only, volume_only, -1));
+  const int rc = check();
+  if (rc != ESDG_B200_OK) return rc;
+  return get_state(ESDG_B200_REG_K, out);
+}
+
+// ---- host-evaluated reductions over the device state -----------------------
+
+template <class F>
+int SolverCore::for_each_element_chunk(int reg, int reg2, F&& f) {
+  const int prec = opt_.precision;
+  const size_t per = size_t(prec) * 5 * size_t(n3_);
+  const int64_t chunk = std::max<int64_t>(1, (int64_t(128) << 20) / int64_t(per));
+  std::vector<char> a, b;
+  for (auto& ls : shards_)
+    for (int64_t first = 0; first < ls.end - ls.begin; first += chunk) {
+      const int64_t count = std::min(chunk, ls.end - ls.begin - first);
+      a.resize(per * size_t(count));
+      RC(ls.dev->download(reg, a.data(), first, count, nullptr, false));
+      if (reg2 >= 0) {
+        b.resize(per * size_t(count));
+        RC(ls.dev->download(reg2, b.data(), first, count, nullptr, false));
+      }
+      f(ls.begin + first, count, a.data(), reg2 >= 0 ? b.data() : nullptr);
+    }
+  return ESDG_B200_OK;
+}
+
+namespace {
+struct Neumaier {
+  double s = 0.0, c = 0.0;
+  void add(double x) {
+    const double t = s + x;
+    c += (std::abs(s) >= std::abs(x)) ? (s - t) + x : (x - t) + s;
+    s = t;
+  }
+  double value() const { return s + c; }
+};
+} // namespace
+
+// compute_stable_dt (time_integration.hpp:55-92), 64-bit, on the downloaded
+// state; startup-only in the reference's runner (runner.cpp:150-153)
+int SolverCore::compute_dt(double courant, double* dt_out) {
+  std::vector<double> gap(static_cast<size_t>(nq_));
+  for (int i = 0; i < nq_; ++i) {
+    double g = 2.0;
+    if (i > 0) g = std::min(g, ref_.nodes[size_t(i)] - ref_.nodes[size_t(i) - 1]);
+    if (i + 1 < nq_) g = std::min(g, ref_.nodes[size_t(i) + 1] - ref_.nodes[size_t(i)]);
+    gap[size_t(i)] = g;
+  }
+  const double hd[3] = {0.5 * mesh_->delta[0], 0.5 * mesh_->delta[1], 0.5 * mesh_->delta[2]};
+  const double gamma = opt_.gas.gamma, grav = opt_.gas.gravity;
+  const int prec = opt_.precision;
+  double dt = std::numeric_limits<double>::infinity();
+  bool bad = false;
+  std::mutex mu;
+  RC(for_each_element_chunk(ESDG_B200_REG_Q, -1, [&](int64_t first, int64_t count, const char* qd, const char*) {
+    parallel_for(count, [&](int64_t b, int64_t e) {
+      double local = std::numeric_limits<double>::infinity();
+      bool local_bad = false;
+      for (int64_t i = b; i < e; ++i)
+        for (int n = 0; n < n3_; ++n) {
+          double q[5];
+          for (int v = 0; v < 5; ++v)
+            q[v] = load_real(qd, (size_t(i) * 5 + size_t(v)) * size_t(n3_) + size_t(n), prec);
+          const int idx[3] = {n % nq_, (n / nq_) % nq_, n / n2_};
+          const double z = mesh_->node_coordinate(first + i, 2, ref_.nodes[size_t(idx[2])]);
+          const double phi = prec == 8 ? grav * z : double(float(grav * z));
+          if (!(q[0] > 0.0)) { local_bad = true; continue; }
+          const double ke = 0.5 * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]) / q[0];
+          const double p = (gamma - 1.0) * (q[4] - ke - q[0] * phi);
+          if (!(p > 0.0)) { local_bad = true; continue; }
+          const double c = std::sqrt(gamma * p / q[0]);
+          for (int d = 0; d < 3; ++d) {
+            const double dx = hd[d] * gap[size_t(idx[d])];
+            const double u = std::abs(q[1 + d] / q[0]);
+            local = std::min(local, dx / (u + c));
+          }
+        }
+      std::lock_guard<std::mutex> lock(mu); // min is order independent
+      dt = std::min(dt, local);
+      bad = bad || local_bad;
+    });
+  }));
+  if (bad) {
+    set_message("compute_dt: non-physical state");
+    return ESDG_B200_NONPHYSICAL;
+  }
+  *dt_out = courant * dt;
+  return ESDG_B200_OK;
+}
+
+// quadrature_total (diagnostics.hpp:30-47): serial Neumaier sum in element /
+// node order, identical to the reference's summation order
+int SolverCore::quadrature_total(int reg, int var, double* out) {
+  if (var < 0 || var > 4 || (reg != 0 && reg != 1)) return ESDG_B200_BADARG;
+  const double J = mesh_->jacobian;
+  const int prec = opt_.precision;
+  Neumaier sum;
+  RC(for_each_element_chunk(reg, -1, [&](int64_t, int64_t count, const char* qd, const char*) {
+    for (int64_t i = 0; i < count; ++i)
+      for (int n = 0; n < n3_; ++n) {
+        const int a = n % nq_, b = (n / nq_) % nq_, c = n / n2_;
+        const double w3 = ref_.weights[size_t(a)] * ref_.weights[size_t(b)] * ref_.weights[size_t(c)];
+        sum.add(J * w3 * load_real(qd, (size_t(i) * 5 + size_t(var)) * size_t(n3_) + size_t(n), prec));
+      }
+  }));
+  *out = sum.value();
+  return ESDG_B200_OK;
+}
+
+// total_entropy (diagnostics.hpp:49-71)
+int SolverCore::total_entropy(double* out) {
+  const double J = mesh_->jacobian, gamma = opt_.gas.gamma, grav = opt_.gas.gravity;
+  const int prec = opt_.precision;
+  Neumaier sum;
+  bool bad = false;
+  RC(for_each_element_chunk(ESDG_B200_REG_Q, -1, [&](int64_t first, int64_t count, const char* qd, const char*) {
+    std::vector<double> eta(size_t(count) * size_t(n3_));
+    parallel_for(count, [&](int64_t b, int64_t e) {
+      for (int64_t i = b; i < e; ++i)
+        for (int n = 0; n < n3_; ++n) {
+          double q[5];
+          for (int v = 0; v < 5; ++v)
+            q[v] = load_real(qd, (size_t(i) * 5 + size_t(v)) * size_t(n3_) + size_t(n), prec);
+          const int a = n % nq_, bb = (n / nq_) % nq_, c = n / n2_;
+          const double z = mesh_->node_coordinate(first + i, 2, ref_.nodes[size_t(c)]);
+          const double phi = prec == 8 ? grav * z : double(float(grav * z));
+          const double ke = 0.5 * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]) / q[0];
+          const double p = (gamma - 1.0) * (q[4] - ke - q[0] * phi);
+          if (!(q[0] > 0.0) || !(p > 0.0)) bad = true;
+          const double s = std::log(p) - gamma * std::log(q[0]);
+          const double w3 = ref_.weights[size_t(a)] * ref_.weights[size_t(bb)] * ref_.weights[size_t(c)];
+          eta[size_t(i) * size_t(n3_) + size_t(n)] = J * w3 * (-q[0] * s / (gamma - 1.0));
+        }
+    });
+    for (double v : eta) sum.add(v);
+  }));
+  if (bad) return ESDG_B200_NONPHYSICAL;
+  *out = sum.value();
+  return ESDG_B200_OK;
+}
+
+// entropy_production (diagnostics.hpp:73-106) of the pair (q register,
+// k register): sum J w^3 v(q) . k
+int SolverCore::entropy_production(double* out) {
+  const double J = mesh_->jacobian, gamma = opt_.gas.gamma, grav = opt_.gas.gravity;
+  const int prec = opt_.precision;
+  Neumaier sum;
+  bool bad = false;
+  RC(for_each_element_chunk(ESDG_B200_REG_Q, ESDG_B200_REG_K, [&](int64_t first, int64_t count, const char* qd, const char* kd) {
+    std::vector<double> term(size_t(count) * size_t(n3_));
+    parallel_for(count, [&](int64_t b, int64_t e) {
+      for (int64_t i = b; i < e; ++i)
+        for (int n = 0; n < n3_; ++n) {
+          double q[5], r[5];
+          for (int v = 0; v < 5; ++v) {
+            q[v] = load_real(qd, (size_t(i) * 5 + size_t(v)) * size_t(n3_) + size_t(n), prec);
+            r[v] = load_real(kd, (size_t(i) * 5 + size_t(v)) * size_t(n3_) + size_t(n), prec);
+          }
+          const int a = n % nq_, bb = (n / nq_) % nq_, c = n / n2_;
+          const double z = mesh_->node_coordinate(first + i, 2, ref_.nodes[size_t(c)]);
+          const double phi = prec == 8 ? grav * z : double(float(grav * z));
+          const double rho = q[0];
+          const double ke = 0.5 * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]) / rho;
+          const double p = (gamma - 1.0) * (q[4] - ke - rho * phi);
+          if (!(rho > 0.0) || !(p > 0.0)) bad = true;
+          const double bq = rho / (2.0 * p);
+          const double u[3] = {q[1] / rho, q[2] / rho, q[3] / rho};
+          const double u2 = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+          const double s = std::log(p) - gamma * std::log(rho);
+          const double vv[5] = {(gamma - s) / (gamma - 1.0) - bq * (u2 - 2.0 * phi),
+                                2.0 * bq * u[0], 2.0 * bq * u[1], 2.0 * bq * u[2], -2.0 * bq};
+          const double w3 = ref_.weights[size_t(a)] * ref_.weights[size_t(bb)] * ref_.weights[size_t(c)];
+          term[size_t(i) * size_t(n3_) + size_t(n)] =
+              J * w3 * (vv[0] * r[0] + vv[1] * r[1] + vv[2] * r[2] + vv[3] * r[3] + vv[4] * r[4]);
+        }
+    });
+    for (double v : term) sum.add(v);
+  }));
+  if (bad) return ESDG_B200_NONPHYSICAL;
+  *out = sum.value();
+  return ESDG_B200_OK;
+}
+
+} // namespace host
+} // namespace esdg_b200

@@ -1,0 +1,121 @@
+// solver_core.hpp -- host driver behind the level-2 C ABI: the GPU
+// counterpart of esdg::Solver<Real> (core/include/esdg/solver.hpp:26-158).
+// Owns one shard per locally held partition and runs the reference's RHS
+// phase order on CUDA streams:
+//   post ghost traces -> volume (overlaps the exchange) -> faces -> update
+// (rhs_job, solver.hpp:240-340).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "esdg_b200.h"
+#include "host_types.hpp"
+#include "../shard_internal.hpp"
+
+namespace esdg_b200 {
+namespace host {
+
+class SolverCore {
+public:
+  struct Options {
+    int order = 4;
+    int precision = 8;
+    esdg_b200_gas gas{};
+    esdg_b200_settings settings{};
+    int world_size = 1;          // number of partitions of the mesh
+    std::vector<int> local_ranks; // partitions held by this process
+    std::vector<int> devices;     // device of each local partition
+    esdg_b200_exchange_fn exchange = nullptr; // set => peers are remote
+    void* exchange_user = nullptr;
+  };
+
+  static int create(Mesh* mesh, const Options& opt, SolverCore** out);
+  ~SolverCore();
+
+  int n3() const { return n3_; }
+  int nq() const { return nq_; }
+  int precision() const { return opt_.precision; }
+  int64_t local_begin() const { return local_begin_; }
+  int64_t local_end() const { return local_end_; }
+  int64_t local_elements() const { return local_end_ - local_begin_; }
+  const RefElement& ref() const { return ref_; }
+  const Mesh& mesh() const { return *mesh_; }
+
+  int set_path(int path);
+  int set_settings(const esdg_b200_settings& s);
+  int halo(int32_t* peer, int64_t* offset, int64_t* count, int capacity) const;
+  ShardBase* shard(size_t i) { return shards_[i].dev.get(); }
+  size_t n_shards() const { return shards_.size(); }
+
+  int init_case(int case_id, uint64_t iparam, const double* dparam);
+  int set_state(int reg, const void* host);
+  int get_state(int reg, void* host);
+  int get_phi(void* host) const;
+
+  int assemble_rhs_host(const void* q, void* out, double a_old, double a_new,
+                        bool volume_only);
+  int rhs(int src, int dst, double a_old, double a_new, bool with_source,
+          bool volume_only, int stage);
+  int axpy(double b);
+  int step(double dt, bool check);
+  int sync();
+  int check();
+  int compute_dt(double courant, double* dt);
+  const esdg_b200_error& last_error() const { return err_; }
+
+  int quadrature_total(int reg, int var, double* out);
+  int total_entropy(double* out);
+  int entropy_production(double* out);
+
+  int enable_timing(bool on);
+  int timers(double seconds[4], int64_t* launches, bool reset);
+
+private:
+  struct LocalShard {
+    int rank = 0;
+    int64_t begin = 0, end = 0;
+    RankHalo halo;
+    std::unique_ptr<ShardBase> dev;
+    cudaStream_t comm = nullptr;
+    cudaEvent_t ev_pack = nullptr, ev_recv = nullptr, ev_surf = nullptr;
+  };
+  struct TimedLaunch {
+    cudaEvent_t a, b;
+    int cls;
+  };
+
+  SolverCore() = default;
+  int build_shard(LocalShard& ls);
+  int local_index_of_rank(int rank) const;
+  int exchange_begin(int src);
+  int exchange_end();
+  template <class F>
+  int timed(LocalShard& ls, int cls, F&& launch);
+  int collect_timers();
+  // downloads register `reg` chunk by chunk and calls f(global_elem, ptr)
+  template <class F>
+  int for_each_element_chunk(int reg, int reg2, F&& f);
+
+  Mesh* mesh_ = nullptr;
+  Options opt_;
+  RefElement ref_;
+  int nq_ = 0, n2_ = 0, n3_ = 0;
+  std::vector<int64_t> range_begin_;
+  int64_t local_begin_ = 0, local_end_ = 0;
+  std::vector<LocalShard> shards_;
+  int path_ = ESDG_B200_PATH_SPLIT;
+  bool any_halo_ = false;
+  esdg_b200_error err_{};
+  bool timing_ = false;
+  std::vector<TimedLaunch> pending_;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> event_pool_;
+  double seconds_[4] = {0, 0, 0, 0};
+};
+
+} // namespace host
+} // namespace esdg_b200

@@ -1,0 +1,555 @@
+// shard.cu -- level-1 C ABI: one element partition resident on one GPU
+// (include/esdg_b200.h, "shard" entry points). Owns device memory, derives
+// the kernel constants exactly like the reference's Operators<Real>
+// (core/include/esdg/kernels.hpp:70-92) and launches K1-K5.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "esdg_b200.h"
+#include "esdg_kernels.cuh"
+#include "esdg_launch.hpp"
+#include "shard_internal.hpp"
+
+namespace esdg_b200 {
+
+thread_local std::string g_last_message;
+
+void set_message(const std::string& m) { g_last_message = m; }
+
+int cuda_fail(cudaError_t e, const char* what) {
+  g_last_message = std::string(what) + ": " + cudaGetErrorString(e);
+  return ESDG_B200_CUDA;
+}
+
+#define CU(call)                                                               \
+  do {                                                                         \
+    cudaError_t e_ = (call);                                                   \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);                        \
+  } while (0)
+
+namespace {
+
+constexpr unsigned long long kNoFlag = ~0ull;
+
+template <class Real>
+class Shard final : public ShardBase {
+public:
+  ~Shard() override { release(); }
+
+  int init(const esdg_b200_shard_desc& d) {
+    nq_ = d.nq;
+    n2_ = nq_ * nq_;
+    n3_ = n2_ * nq_;
+    ne_ = d.n_elements;
+    elem_offset_ = d.elem_offset;
+    device_ = d.device;
+    n_ghost_ = d.n_ghost;
+    n_send_ = d.n_send;
+    dissipation_ = d.dissipation;
+    coriolis_mode_ = d.coriolis_mode;
+    CU(cudaSetDevice(device_));
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, device_));
+    if (prop.major < 10) {
+      set_message("esdg_b200 needs an sm_100 class GPU (found sm_" +
+                  std::to_string(prop.major) + std::to_string(prop.minor) + ")");
+      return ESDG_B200_CUDA;
+    }
+    CU(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+
+    // Operators<Real> (kernels.hpp:79-91): 64-bit operators rounded to Real
+    std::vector<Real> D(static_cast<size_t>(n2_)), w(static_cast<size_t>(nq_));
+    for (int i = 0; i < n2_; ++i) D[size_t(i)] = Real(d.diff[i]);
+    for (int i = 0; i < nq_; ++i) w[size_t(i)] = Real(d.weights[i]);
+    for (int k = 0; k < 3; ++k) {
+      metric_[k] = Real(d.metric[k]);
+      lift_[k] = metric_[k] / w[0];
+    }
+    negc_.assign(size_t(3 * n2_), Real(0));
+    for (int k = 0; k < 3; ++k)
+      for (int i = 0; i < n2_; ++i)
+        negc_[size_t(k * n2_ + i)] = -(Real(2) * metric_[k] * D[size_t(i)]);
+    const Real gamma = Real(d.gamma), R = Real(d.gas_R);
+    gas_.gamma = gamma;
+    gas_.gm1 = gamma - Real(1);
+    gas_.cg = Real(1) / (Real(2) * (gamma - Real(1)));
+    gas_.igm1 = Real(1) / (gamma - Real(1));
+    gas_.Rgas = R;
+    gas_.half_over_gamma = Real(1) / (Real(2) * gamma);
+    gas_.gm1_over_gamma = (gamma - Real(1)) / gamma;
+    gas_.half_over_R = Real(1) / (Real(2) * R);
+
+    const size_t state_bytes = sizeof(Real) * size_t(ne_) * 5 * size_t(n3_);
+    CU(cudaMalloc(&q_, state_bytes ? state_bytes : 16));
+    CU(cudaMalloc(&k_, state_bytes ? state_bytes : 16));
+    CU(cudaMemset(q_, 0, state_bytes));
+    CU(cudaMemset(k_, 0, state_bytes));
+    CU(alloc_copy(&phi_, d.phi, sizeof(Real) * size_t(ne_) * size_t(n3_)));
+    CU(alloc_copy(&nbr_, d.nbr, sizeof(int32_t) * size_t(ne_) * 6));
+    CU(alloc_copy(&ghost_phi_, d.ghost_phi,
+                  sizeof(Real) * size_t(n_ghost_) * size_t(n2_)));
+    CU(alloc_copy(&send_elem_, d.send_elem, sizeof(int32_t) * size_t(n_send_)));
+    CU(alloc_copy(&send_face_, d.send_face, sizeof(int32_t) * size_t(n_send_)));
+    const size_t halo = sizeof(Real) * 5 * size_t(n2_);
+    CU(cudaMalloc(&recv_, n_ghost_ ? halo * size_t(n_ghost_) : 16));
+    CU(cudaMalloc(&send_, n_send_ ? halo * size_t(n_send_) : 16));
+    CU(cudaMemset(recv_, 0, n_ghost_ ? halo * size_t(n_ghost_) : 16));
+    if (coriolis_mode_ != 0) {
+      if (!d.elem_ylevel || !d.coriolis_f || d.n_ylevels < 1) {
+        set_message("coriolis_mode != 0 needs elem_ylevel and coriolis_f");
+        return ESDG_B200_BADARG;
+      }
+      CU(alloc_copy(&ylevel_, d.elem_ylevel, sizeof(int32_t) * size_t(ne_)));
+      CU(alloc_copy(&cor_f_, d.coriolis_f,
+                    sizeof(Real) * size_t(d.n_ylevels) * size_t(nq_)));
+    }
+    CU(cudaMalloc(&flag_, sizeof(unsigned long long)));
+    CU(cudaMemcpy(flag_, &kNoFlag, sizeof kNoFlag, cudaMemcpyHostToDevice));
+    CU(cudaMallocHost(&flag_host_, sizeof(unsigned long long)));
+    return ESDG_B200_OK;
+  }
+
+  int upload(int reg, const void* host, int64_t first, int64_t count,
+             cudaStream_t st, bool async) override {
+    if (!range_ok(reg, first, count) || !host) return bad("upload: bad range");
+    CU(cudaSetDevice(device_));
+    const size_t per = sizeof(Real) * 5 * size_t(n3_);
+    Real* dst = reg_ptr(reg) + size_t(first) * 5 * size_t(n3_);
+    if (async)
+      CU(cudaMemcpyAsync(dst, host, per * size_t(count), cudaMemcpyHostToDevice, pick(st)));
+    else
+      CU(cudaMemcpy(dst, host, per * size_t(count), cudaMemcpyHostToDevice));
+    return ESDG_B200_OK;
+  }
+
+  int download(int reg, void* host, int64_t first, int64_t count,
+               cudaStream_t st, bool async) override {
+    if (!range_ok(reg, first, count) || !host) return bad("download: bad range");
+    CU(cudaSetDevice(device_));
+    const size_t per = sizeof(Real) * 5 * size_t(n3_);
+    const Real* src = reg_ptr(reg) + size_t(first) * 5 * size_t(n3_);
+    if (async) {
+      CU(cudaMemcpyAsync(host, src, per * size_t(count), cudaMemcpyDeviceToHost, pick(st)));
+    } else {
+      CU(cudaStreamSynchronize(stream_));
+      CU(cudaMemcpy(host, src, per * size_t(count), cudaMemcpyDeviceToHost));
+    }
+    return ESDG_B200_OK;
+  }
+
+  void* register_ptr(int reg) override {
+    return (reg == 0 || reg == 1) ? reg_ptr(reg) : nullptr;
+  }
+  void* send_ptr() override { return send_; }
+  void* recv_ptr() override { return recv_; }
+  cudaStream_t stream() override { return stream_; }
+  int device() const override { return device_; }
+  int64_t n_elements() const override { return ne_; }
+  int64_t n_ghost() const override { return n_ghost_; }
+  int64_t n_send() const override { return n_send_; }
+  size_t trace_bytes() const override { return sizeof(Real) * 5 * size_t(n2_); }
+  int64_t launch_count() const override { return launches_; }
+  void set_dissipation(int on) override { dissipation_ = on; }
+
+  int pack(int src, cudaStream_t st) override {
+    if (src != 0 && src != 1) return bad("pack: bad register");
+    if (n_send_ == 0) return ESDG_B200_OK;
+    CU(cudaSetDevice(device_));
+    cudaError_t e = cudaErrorInvalidValue;
+    switch (nq_) {
+#define ESDG_CASE(NQ)                                                          \
+  case NQ:                                                                     \
+    e = launch_pack<Real, NQ>(reg_ptr(src), send_elem_, send_face_, send_,     \
+                              n_send_, pick(st));                              \
+    break;
+      ESDG_CASE(2) ESDG_CASE(3) ESDG_CASE(4) ESDG_CASE(5) ESDG_CASE(6)
+      ESDG_CASE(7) ESDG_CASE(8)
+#undef ESDG_CASE
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "pack_kernel");
+    ++launches_;
+    return ESDG_B200_OK;
+  }
+
+  int rhs(int mode, int src, int dst, double a_old, double a_new,
+          int with_source, int stage, cudaStream_t st) override {
+    if ((src != 0 && src != 1) || (dst != 0 && dst != 1) || src == dst)
+      return bad("rhs: src and dst must be distinct registers 0/1");
+    CU(cudaSetDevice(device_));
+    cudaError_t e = cudaErrorInvalidValue;
+    switch (nq_) {
+#define ESDG_CASE(NQ)                                                          \
+  case NQ:                                                                     \
+    e = run_rhs<NQ>(mode, src, dst, a_old, a_new, with_source, stage,          \
+                    pick(st));                                                 \
+    break;
+      ESDG_CASE(2) ESDG_CASE(3) ESDG_CASE(4) ESDG_CASE(5) ESDG_CASE(6)
+      ESDG_CASE(7) ESDG_CASE(8)
+#undef ESDG_CASE
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "rhs_kernel");
+    if (ne_ > 0) ++launches_;
+    return ESDG_B200_OK;
+  }
+
+  int axpy(double b, cudaStream_t st) override {
+    CU(cudaSetDevice(device_));
+    const cudaError_t e = launch_axpy<Real>(
+        q_, k_, Real(b), static_cast<long long>(ne_) * 5 * n3_, pick(st));
+    if (e != cudaSuccess) return cuda_fail(e, "axpy_kernel");
+    if (ne_ > 0) ++launches_;
+    return ESDG_B200_OK;
+  }
+
+  int check(cudaStream_t st, int src, esdg_b200_error* err) override {
+    CU(cudaSetDevice(device_));
+    cudaStream_t s = pick(st);
+    CU(cudaMemcpyAsync(flag_host_, flag_, sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    const unsigned long long key = *flag_host_;
+    if (err) std::memset(err, 0, sizeof *err);
+    if (key == kNoFlag) return ESDG_B200_OK;
+    CU(cudaMemcpyAsync(flag_, &kNoFlag, sizeof kNoFlag, cudaMemcpyHostToDevice, s));
+    CU(cudaStreamSynchronize(s));
+    const int stage = int(key >> 56);
+    const int64_t elem = int64_t((key >> 10) & ((1ull << 46) - 1));
+    const int node = int(key & 1023ull);
+    if (err) {
+      err->set = 1;
+      err->element = elem;
+      err->node = node;
+      err->stage = stage;
+      // payload: re-evaluate compute_node_vals' checks (physics.hpp:56-74) on
+      // the flagged node of the source register, in Real arithmetic
+      const int64_t le = elem - elem_offset_;
+      Real qv[5] = {0, 0, 0, 0, 0}, ph = 0;
+      if (le >= 0 && le < ne_) {
+        for (int v = 0; v < 5; ++v)
+          CU(cudaMemcpy(&qv[v],
+                        reg_ptr(src) + (size_t(le) * 5 + size_t(v)) * size_t(n3_) + node,
+                        sizeof(Real), cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(&ph, phi_ + size_t(le) * size_t(n3_) + node, sizeof(Real),
+                      cudaMemcpyDeviceToHost));
+      }
+      err->rho = double(qv[0]);
+      err->pressure = 0.0;
+      if (qv[0] > Real(0)) {
+        const Real inv = Real(1) / qv[0];
+        const Real u0 = qv[1] * inv, u1 = qv[2] * inv, u2 = qv[3] * inv;
+        const Real ke = Real(0.5) * (qv[1] * u0 + qv[2] * u1 + qv[3] * u2);
+        err->pressure = double(gas_.gm1 * (qv[4] - ke - qv[0] * ph));
+      }
+    }
+    return ESDG_B200_NONPHYSICAL;
+  }
+
+private:
+  template <int NQ>
+  cudaError_t run_rhs(int mode, int src, int dst, double a_old, double a_new,
+                      int with_source, int stage, cudaStream_t st) {
+    dev::RhsParams<Real, NQ> P;
+    P.q = reg_ptr(src);
+    P.out = reg_ptr(dst);
+    P.phi = phi_;
+    P.nbr = nbr_;
+    P.ghost_q = recv_;
+    P.ghost_phi = ghost_phi_;
+    P.ylevel = ylevel_;
+    P.cor_f = cor_f_;
+    P.flag = flag_;
+    P.ne = ne_;
+    P.elem_offset = elem_offset_;
+    P.a_old = Real(a_old);
+    P.a_new = Real(a_new);
+    P.gas = gas_;
+    for (int k = 0; k < 3; ++k) {
+      for (int i = 0; i < NQ * NQ; ++i)
+        P.negc[k][i] = negc_[size_t(k * NQ * NQ + i)];
+      P.lift[k] = lift_[k];
+    }
+    P.with_source = (with_source && coriolis_mode_ != 0) ? 1 : 0;
+    P.dissipation = dissipation_;
+    P.stage = stage;
+    return launch_rhs<Real, NQ>(mode, P, st);
+  }
+
+  static cudaError_t alloc_copy_impl(void** dst, const void* src, size_t bytes) {
+    cudaError_t e = cudaMalloc(dst, bytes ? bytes : 16);
+    if (e != cudaSuccess) return e;
+    if (bytes && src) e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+    return e;
+  }
+  template <class T>
+  static cudaError_t alloc_copy(T** dst, const void* src, size_t bytes) {
+    return alloc_copy_impl(reinterpret_cast<void**>(dst), src, bytes);
+  }
+
+  Real* reg_ptr(int reg) { return reg == 0 ? q_ : k_; }
+  cudaStream_t pick(cudaStream_t st) { return st ? st : stream_; }
+  bool range_ok(int reg, int64_t first, int64_t count) const {
+    return (reg == 0 || reg == 1) && first >= 0 && count >= 0 &&
+           first + count <= ne_;
+  }
+  int bad(const char* m) {
+    set_message(m);
+    return ESDG_B200_BADARG;
+  }
+
+  void release() {
+    if (device_ >= 0) cudaSetDevice(device_);
+    cudaFree(q_);
+    cudaFree(k_);
+    cudaFree(phi_);
+    cudaFree(nbr_);
+    cudaFree(ghost_phi_);
+    cudaFree(send_elem_);
+    cudaFree(send_face_);
+    cudaFree(recv_);
+    cudaFree(send_);
+    cudaFree(ylevel_);
+    cudaFree(cor_f_);
+    cudaFree(flag_);
+    if (flag_host_) cudaFreeHost(flag_host_);
+    if (stream_) cudaStreamDestroy(stream_);
+  }
+
+  int nq_ = 0, n2_ = 0, n3_ = 0, device_ = -1;
+  int64_t ne_ = 0, elem_offset_ = 0, n_ghost_ = 0, n_send_ = 0;
+  int dissipation_ = 1, coriolis_mode_ = 0;
+  Real metric_[3] = {0, 0, 0}, lift_[3] = {0, 0, 0};
+  std::vector<Real> negc_;
+  dev::GasParams<Real> gas_{};
+  Real *q_ = nullptr, *k_ = nullptr, *phi_ = nullptr, *ghost_phi_ = nullptr;
+  Real *recv_ = nullptr, *send_ = nullptr, *cor_f_ = nullptr;
+  int32_t *nbr_ = nullptr, *send_elem_ = nullptr, *send_face_ = nullptr,
+          *ylevel_ = nullptr;
+  unsigned long long *flag_ = nullptr, *flag_host_ = nullptr;
+  cudaStream_t stream_ = nullptr;
+  int64_t launches_ = 0;
+};
+
+// ---- FMA peak micro-benchmark (roofline denominator of K1) ----------------
+
+template <class Real>
+__global__ void __launch_bounds__(256) fma_peak_kernel(Real* out, int iters) {
+  Real a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = Real(threadIdx.x + i) * Real(1e-3);
+  // register operands (not immediates): the figure wanted is the 3-register
+  // FMA rate the flux code runs at
+  const Real m = Real(1) - Real(1e-6) * Real(1 + (iters & 1));
+  const Real c = Real(1e-6) * Real(1 + (iters & 2));
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = dev::fma_(a[i], m, c);
+    }
+  }
+  Real s = Real(0);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == Real(123.456)) out[0] = s; // keeps the chain alive
+}
+
+template <class Real>
+int measure_peak(int device, double* tflops) {
+  CU(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, device));
+  Real* out = nullptr;
+  CU(cudaMalloc(&out, sizeof(Real)));
+  const int blocks = prop.multiProcessorCount * 8, threads = 256, iters = 4096;
+  cudaEvent_t t0, t1;
+  CU(cudaEventCreate(&t0));
+  CU(cudaEventCreate(&t1));
+  double best = 0.0;
+  for (int rep = 0; rep < 5; ++rep) {
+    CU(cudaEventRecord(t0));
+    fma_peak_kernel<Real><<<blocks, threads>>>(out, iters);
+    CU(cudaEventRecord(t1));
+    CU(cudaEventSynchronize(t1));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, t0, t1));
+    const double flops = 2.0 * 64.0 * double(iters) * double(blocks) * threads;
+    const double tf = flops / (double(ms) * 1e-3) / 1e12;
+    if (rep > 0 && tf > best) best = tf;
+  }
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  cudaFree(out);
+  *tflops = best;
+  return ESDG_B200_OK;
+}
+
+} // namespace
+
+int create_shard(const esdg_b200_shard_desc& d, ShardBase** out) {
+  if (d.nq < 2 || d.nq > 8 || d.n_elements < 0 || !d.diff || !d.weights ||
+      (d.n_elements > 0 && (!d.nbr || !d.phi)) ||
+      (d.n_ghost > 0 && !d.ghost_phi) ||
+      (d.n_send > 0 && (!d.send_elem || !d.send_face))) {
+    set_message("shard_create: bad descriptor");
+    return ESDG_B200_BADARG;
+  }
+  if (d.n_elements >= (int64_t(1) << 31)) {
+    set_message("shard_create: more than 2^31 elements in one partition");
+    return ESDG_B200_BADARG;
+  }
+  int rc;
+  if (d.precision == 8) {
+    auto* s = new Shard<double>();
+    rc = s->init(d);
+    if (rc != ESDG_B200_OK) {
+      delete s;
+      return rc;
+    }
+    *out = s;
+  } else if (d.precision == 4) {
+    auto* s = new Shard<float>();
+    rc = s->init(d);
+    if (rc != ESDG_B200_OK) {
+      delete s;
+      return rc;
+    }
+    *out = s;
+  } else {
+    set_message("shard_create: precision must be 8 or 4");
+    return ESDG_B200_BADARG;
+  }
+  return ESDG_B200_OK;
+}
+
+} // namespace esdg_b200
+
+using esdg_b200::ShardBase;
+
+struct esdg_b200_shard {
+  ShardBase* impl;
+  int last_src;
+};
+
+extern "C" {
+
+int esdg_b200_abi_version(void) { return ESDG_B200_ABI_VERSION; }
+
+const char* esdg_b200_last_message(void) {
+  return esdg_b200::g_last_message.c_str();
+}
+
+int esdg_b200_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int esdg_b200_shard_create(const esdg_b200_shard_desc* desc,
+                           esdg_b200_shard** out) {
+  if (!desc || !out) return ESDG_B200_BADARG;
+  ShardBase* impl = nullptr;
+  const int rc = esdg_b200::create_shard(*desc, &impl);
+  if (rc != ESDG_B200_OK) return rc;
+  *out = new esdg_b200_shard{impl, 0};
+  return ESDG_B200_OK;
+}
+
+void esdg_b200_shard_destroy(esdg_b200_shard* s) {
+  if (!s) return;
+  delete s->impl;
+  delete s;
+}
+
+int esdg_b200_shard_upload(esdg_b200_shard* s, int reg, const void* host,
+                           int64_t first, int64_t count) {
+  return s ? s->impl->upload(reg, host, first, count, nullptr, false)
+           : ESDG_B200_BADARG;
+}
+int esdg_b200_shard_download(esdg_b200_shard* s, int reg, void* host,
+                             int64_t first, int64_t count) {
+  return s ? s->impl->download(reg, host, first, count, nullptr, false)
+           : ESDG_B200_BADARG;
+}
+int esdg_b200_shard_upload_async(esdg_b200_shard* s, int reg, const void* host,
+                                 int64_t first, int64_t count, void* stream) {
+  return s ? s->impl->upload(reg, host, first, count, cudaStream_t(stream), true)
+           : ESDG_B200_BADARG;
+}
+int esdg_b200_shard_download_async(esdg_b200_shard* s, int reg, void* host,
+                                   int64_t first, int64_t count, void* stream) {
+  return s ? s->impl->download(reg, host, first, count, cudaStream_t(stream), true)
+           : ESDG_B200_BADARG;
+}
+void* esdg_b200_shard_register_ptr(esdg_b200_shard* s, int reg) {
+  return s ? s->impl->register_ptr(reg) : nullptr;
+}
+void* esdg_b200_shard_send_ptr(esdg_b200_shard* s) {
+  return s ? s->impl->send_ptr() : nullptr;
+}
+void* esdg_b200_shard_recv_ptr(esdg_b200_shard* s) {
+  return s ? s->impl->recv_ptr() : nullptr;
+}
+void* esdg_b200_shard_stream(esdg_b200_shard* s) {
+  return s ? s->impl->stream() : nullptr;
+}
+
+int esdg_b200_shard_pack(esdg_b200_shard* s, int src, void* stream) {
+  return s ? s->impl->pack(src, cudaStream_t(stream)) : ESDG_B200_BADARG;
+}
+
+int esdg_b200_shard_volume(esdg_b200_shard* s, int src, int dst, double a_old,
+                           double a_new, int with_source, int stage,
+                           void* stream) {
+  if (!s) return ESDG_B200_BADARG;
+  s->last_src = src;
+  return s->impl->rhs(esdg_b200::kModeVolume, src, dst, a_old, a_new,
+                      with_source, stage, cudaStream_t(stream));
+}
+
+int esdg_b200_shard_surface(esdg_b200_shard* s, int src, int dst, double a_new,
+                            int stage, void* stream) {
+  if (!s) return ESDG_B200_BADARG;
+  s->last_src = src;
+  return s->impl->rhs(esdg_b200::kModeSurface, src, dst, 1.0, a_new, 0, stage,
+                      cudaStream_t(stream));
+}
+
+int esdg_b200_shard_rhs_fused(esdg_b200_shard* s, int src, int dst,
+                              double a_old, double a_new, int stage,
+                              void* stream) {
+  if (!s) return ESDG_B200_BADARG;
+  s->last_src = src;
+  return s->impl->rhs(esdg_b200::kModeFused, src, dst, a_old, a_new, 1, stage,
+                      cudaStream_t(stream));
+}
+
+int esdg_b200_shard_axpy(esdg_b200_shard* s, double b, void* stream) {
+  return s ? s->impl->axpy(b, cudaStream_t(stream)) : ESDG_B200_BADARG;
+}
+
+int esdg_b200_shard_check(esdg_b200_shard* s, void* stream,
+                          esdg_b200_error* err) {
+  return s ? s->impl->check(cudaStream_t(stream), s->last_src, err)
+           : ESDG_B200_BADARG;
+}
+
+int64_t esdg_b200_shard_launch_count(const esdg_b200_shard* s) {
+  return s ? s->impl->launch_count() : 0;
+}
+
+int esdg_b200_measure_fma_peak(int device, int precision, double* tflops) {
+  if (!tflops) return ESDG_B200_BADARG;
+  if (precision == 8) return esdg_b200::measure_peak<double>(device, tflops);
+  if (precision == 4) return esdg_b200::measure_peak<float>(device, tflops);
+  return ESDG_B200_BADARG;
+}
+
+} // extern "C"

@@ -1,0 +1,44 @@
+// shard_internal.hpp -- precision-erased interface of one device partition,
+// shared by shard.cu (implementation) and gpu_solver.cpp (host driver).
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "esdg_b200.h"
+
+namespace esdg_b200 {
+
+class ShardBase {
+public:
+  virtual ~ShardBase() = default;
+  virtual int upload(int reg, const void* host, int64_t first, int64_t count,
+                     cudaStream_t st, bool async) = 0;
+  virtual int download(int reg, void* host, int64_t first, int64_t count,
+                       cudaStream_t st, bool async) = 0;
+  virtual void* register_ptr(int reg) = 0;
+  virtual void* send_ptr() = 0;
+  virtual void* recv_ptr() = 0;
+  virtual cudaStream_t stream() = 0;
+  virtual int device() const = 0;
+  virtual int64_t n_elements() const = 0;
+  virtual int64_t n_ghost() const = 0;
+  virtual int64_t n_send() const = 0;
+  virtual size_t trace_bytes() const = 0;
+  virtual int64_t launch_count() const = 0;
+  virtual void set_dissipation(int on) = 0;
+  virtual int pack(int src, cudaStream_t st) = 0;
+  // mode: RhsMode (esdg_launch.hpp)
+  virtual int rhs(int mode, int src, int dst, double a_old, double a_new,
+                  int with_source, int stage, cudaStream_t st) = 0;
+  virtual int axpy(double b, cudaStream_t st) = 0;
+  virtual int check(cudaStream_t st, int src, esdg_b200_error* err) = 0;
+};
+
+int create_shard(const esdg_b200_shard_desc& d, ShardBase** out);
+void set_message(const std::string& m);
+int cuda_fail(cudaError_t e, const char* what);
+
+} // namespace esdg_b200

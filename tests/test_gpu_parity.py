@@ -1,0 +1,288 @@
+"""GPU parity: the CUDA path, called through the C ABI, against the CPU
+oracle on identical inputs (-m gpu). Tolerances are stated per test.
+
+FP64 RHS tolerance: max_v max|d rhs_v| / S_v <= 2e-11 with S_v the abs-sum
+flux scale. Why not 1e-12: the reference forms logarithmic means and entropy
+jumps from DIFFERENCES of per-node logarithms (log_mean.hpp:62,
+physics.hpp:193-194); a 1-ulp difference between the device log and glibc's
+is amplified by 1/(2 xi) (xi = relative jump) in the means and by c T h ~ 4e7
+in the dissipation's energy slot. The reference itself moves by 1.2e-12 of
+max|rhs| when merely recompiled with FMA contraction.
+"""
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+from paper_2605_16684_b200 import capi
+from helpers import both_configs, gas_pair, max_rel_diff, scaled_error, settings_pair, state_error
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 2e-11   # of the abs-sum flux scale
+TOL32 = 5e-6    # FP32 GPU vs FP32 CPU
+
+
+def make(port, kind, margs, order, prec="f64", diss=True, cor=(0, 0.0, 0.0, 0.0), gravity=9.81,
+         ranks=1, path=capi.PATH_SPLIT):
+    oc, cc = both_configs(kind, *margs)
+    so, sc = settings_pair(diss, *cor)
+    go, gc = gas_pair(gravity)
+    osolver = port.mesh(oc).solver(order, prec, gas=go, settings=so)
+    gsolver = capi.GpuSolver(capi.Mesh(cc), order, prec, gas=gc, settings=sc, ranks=ranks)
+    gsolver.set_path(path)
+    return osolver, gsolver
+
+
+CASES = [
+    # kind, mesh args, order, case, seed
+    ("bubble", (3, False), 4, po.CASE_BUBBLE_SHARP, 0),     # BASELINE.json configs[0]
+    ("bubble", (1, True), 4, po.CASE_ENTROPY_TEST, 20240501),
+    ("bubble", (1, True), 2, po.CASE_ENTROPY_TEST, 11),
+    ("bubble", (1, True), 3, po.CASE_ENTROPY_TEST, 22),
+    ("bubble", (2, False), 5, po.CASE_BUBBLE_SMOOTH, 0),
+    ("bubble", (1, False), 6, po.CASE_ENTROPY_TEST, 33),
+    ("bubble", (1, True), 7, po.CASE_ENTROPY_TEST, 44),
+    ("bubble", (1, True), 1, po.CASE_ENTROPY_TEST, 55),
+    ("raw", ((3, 1, 2), 1, (0., 0., 0.), (3e3, 1e3, 2e3), (0, 1, 0)), 4, po.CASE_ENTROPY_TEST, 7),
+]
+
+
+@pytest.mark.parametrize("path", [capi.PATH_SPLIT, capi.PATH_FUSED])
+@pytest.mark.parametrize("kind,margs,order,case,seed", CASES)
+def test_rhs_fp64(port, kind, margs, order, case, seed, path):
+    o, g = make(port, kind, margs, order, path=path)
+    q = o.init_case(case, seed).copy()
+    want = o.assemble_rhs(q)
+    got = g.assemble_rhs(q)
+    scale = o.flux_scale(q)
+    err = scaled_error(got, want, scale)
+    assert err <= TOL64, f"scaled error {err:.3e}"
+
+
+@pytest.mark.parametrize("order", [2, 4, 5])
+def test_volume_rhs_fp64(port, order):
+    o, g = make(port, "bubble", (1, True), order, diss=False)
+    q = o.init_case(po.CASE_ENTROPY_TEST, 11).copy()
+    want, got = o.volume_rhs(q), g.volume_rhs(q)
+    # the reference's own bar between CPU variants is 1e-13 max_rel_diff
+    # (test_kernels.cpp:69-93) and recompiling it with FMA contraction already
+    # moves it by 1.2e-12; device logs + FMAs: 5e-12
+    assert max_rel_diff(want, got) <= 5e-12
+    assert scaled_error(got, want, o.flux_scale(q)) <= TOL64
+
+
+@pytest.mark.parametrize("path", [capi.PATH_SPLIT, capi.PATH_FUSED])
+def test_accumulate_form(port, path):
+    """out <- a_old out + a_new RHS(q) (solver.hpp:112-119, 217-221)."""
+    o, g = make(port, "bubble", (1, True), 4, path=path)
+    q = o.init_case(po.CASE_ENTROPY_TEST, 5).copy()
+    rng = np.random.default_rng(3)
+    out0 = rng.standard_normal(q.shape) * 10.0
+    want = o.assemble_rhs(q, out0.copy(), -0.41789, 0.0625)
+    got = g.assemble_rhs(q, out0.copy(), -0.41789, 0.0625)
+    scale = 0.0625 * o.flux_scale(q) + 10.0
+    assert scaled_error(got, want, scale) <= TOL64
+
+
+def test_a_old_zero_never_reads_out(port):
+    o, g = make(port, "bubble", (1, True), 3)
+    q = o.init_case(po.CASE_ENTROPY_TEST, 9).copy()
+    poison = np.full(q.shape, np.nan)
+    got = g.assemble_rhs(q, poison, 0.0, 1.0)
+    assert np.isfinite(got).all()
+
+
+@pytest.mark.parametrize("path", [capi.PATH_SPLIT, capi.PATH_FUSED])
+def test_coriolis_beta_plane(port, path):
+    cor = (2, 1e-4, 1.6e-11, 3e6)
+    margs = ((2, 1, 1), 1, (0., 0., 0.), (4e6, 6e6, 3e4), (0, 1, 1))
+    o, g = make(port, "raw", margs, 4, cor=cor, path=path)
+    q = o.init_case(po.CASE_ENTROPY_TEST, 13).copy()
+    want, got = o.assemble_rhs(q), g.assemble_rhs(q)
+    assert scaled_error(got, want, o.flux_scale(q) + 1e-4 * np.abs(q).max(axis=(0, 2))) <= TOL64
+
+
+@pytest.mark.parametrize("path", [capi.PATH_SPLIT, capi.PATH_FUSED])
+def test_hydrostatic_rest_exact_zero(port, path):
+    """test_kernels.cpp:254-265: mass and energy tendencies are exactly 0."""
+    o, g = make(port, "bubble", (1, False), 4, path=path)
+    q = o.init_case(po.CASE_HYDROSTATIC).copy()
+    got = g.assemble_rhs(q)
+    assert np.abs(got[:, 0]).max() == 0.0
+    assert np.abs(got[:, 4]).max() == 0.0
+    assert np.abs(got[:, 3]).max() > 0.0
+
+
+@pytest.mark.parametrize("order", [2, 3, 4])
+def test_free_stream(port, order):
+    """test_kernels.cpp:30-44: constant state, phi = 0, periodic."""
+    o, g = make(port, "unit", (1,), order, gravity=0.0)
+    q = o.init_case(po.CASE_CONSTANT, 0, [1.2, 20.0, 10.0, 5.0, 1e5]).copy()
+    got = g.assemble_rhs(q)
+    scale = 2.0 * (2.0 / 0.5) * 10.0 * 1e5
+    assert np.abs(got).max() <= 1e-13 * scale
+
+
+def test_entropy_conservation_and_dissipation(port):
+    """test_kernels.cpp:202-252 / acceptance 1-2 on the GPU tendency."""
+    o, g = make(port, "bubble", (1, True), 4, diss=False)
+    q = o.init_case(po.CASE_ENTROPY_TEST, 2024).copy()
+    rhs = g.assemble_rhs(q)
+    eta = o.total_entropy(q)
+    prod = o.entropy_production(q, rhs)
+    assert abs(prod) <= 1e-10 * abs(eta)
+    want = o.entropy_production(q, o.assemble_rhs(q))
+    # both are roundoff residuals of a cancelling sum; compare on its scale
+    assert abs(prod - want) <= 1e-12 * abs(eta) * 1e-2 + 1e-6
+
+
+def test_discrete_conservation(port):
+    """test_kernels.cpp:164-183: mass and energy rates vanish to 1e-12."""
+    o, g = make(port, "bubble", (1, True), 4)
+    q = o.init_case(po.CASE_ENTROPY_TEST, 99).copy()
+    rhs = g.assemble_rhs(q)
+    for var in (0, 4):
+        rate = o.quadrature_total(rhs, var)
+        scale = o.quadrature_total(np.abs(rhs), var)
+        assert abs(rate) <= 1e-12 * scale
+
+
+@pytest.mark.parametrize("ranks", [2, 4])
+@pytest.mark.parametrize("path", [capi.PATH_SPLIT, capi.PATH_FUSED])
+def test_partition_bitwise_rhs(port, ranks, path):
+    """test_partition.cpp:102-114: the RHS is bitwise independent of the
+    partition count (here: partitions as shards with a real halo exchange)."""
+    _, g1 = make(port, "bubble", (1, True), 4, path=path)
+    o, gn = make(port, "bubble", (1, True), 4, ranks=ranks, path=path)
+    q = o.init_case(po.CASE_ENTROPY_TEST, 31).copy()
+    a, b = g1.assemble_rhs(q), gn.assemble_rhs(q)
+    assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("ranks", [2, 4])
+def test_partition_bitwise_trajectory(port, ranks):
+    """test_partition.cpp:94-100: 10 steps, order 3, bubble_mesh(1)."""
+    states = []
+    for r in (1, ranks):
+        o, g = make(port, "bubble", (1, False), 3, ranks=r)
+        q = o.init_case(po.CASE_BUBBLE_SHARP).copy()
+        g.set_state(q)
+        dt = o.compute_dt(0.5)
+        for _ in range(10):
+            g.step(dt)
+        states.append(g.get_state())
+    assert np.array_equal(states[0], states[1])
+
+
+@pytest.mark.parametrize("path", [capi.PATH_SPLIT, capi.PATH_FUSED])
+def test_trajectory_config1(port, path):
+    """BASELINE.json configs[0]: 10 RK steps of the sharp bubble, N=4, 8^3.
+    Tolerance: rho, E to 1e-12 of max|q_v|; momenta are
+    O(1e-4) against flux scales of O(1e4) -> 1e-9 of max|q_v|."""
+    o, g = make(port, "bubble", (3, False), 4, path=path)
+    q = o.init_case(po.CASE_BUBBLE_SHARP).copy()
+    g.set_state(q)
+    dt = o.compute_dt(0.5)
+    assert abs(g.compute_dt(0.5) - dt) <= 1e-15 * dt
+    for _ in range(10):
+        o.step(dt)
+        g.step(dt)
+    err = state_error(g.get_state(), o.state)
+    assert err[0] <= 1e-12 and err[4] <= 1e-12, err
+    assert max(err[1:4]) <= 1e-9, err
+    # conserved integrals: identical to the reference's to 1e-14
+    gs = g.get_state()
+    for var in (0, 4):
+        a, b = o.quadrature_total(o.state, var), o.quadrature_total(gs, var)
+        assert abs(a - b) <= 1e-14 * abs(a)
+    # entropy production of the GPU state/tendency against the oracle's
+    p_gpu = o.entropy_production(gs, g.assemble_rhs(gs))
+    p_cpu = o.entropy_production(o.state.copy(), o.assemble_rhs(o.state.copy()))
+    assert p_gpu < 0.0
+    assert abs(p_gpu - p_cpu) <= 1e-6 * abs(p_cpu) + 1e-9
+
+
+@pytest.mark.parametrize("path", [capi.PATH_SPLIT, capi.PATH_FUSED])
+@pytest.mark.parametrize("order,case,seed", [(4, po.CASE_ENTROPY_TEST, 20240501), (2, po.CASE_ENTROPY_TEST, 3),
+                                             (7, po.CASE_ENTROPY_TEST, 4), (4, po.CASE_BUBBLE_SMOOTH, 0)])
+def test_rhs_fp32(port, order, case, seed, path):
+    margs = (1, True) if case == po.CASE_ENTROPY_TEST else (2, False)
+    o, g = make(port, "bubble", margs, order, prec="f32", path=path)
+    q = o.init_case(case, seed).copy()
+    want, got = o.assemble_rhs(q), g.assemble_rhs(q)
+    assert scaled_error(got, want, o.flux_scale(q)) <= TOL32
+
+
+def test_trajectory_fp32(port):
+    """FP32 10-step state within 1e-4 of max|q_v|."""
+    o, g = make(port, "bubble", (2, False), 4, prec="f32")
+    q = o.init_case(po.CASE_BUBBLE_SHARP).copy()
+    g.set_state(q)
+    dt = o.compute_dt(0.5)
+    for _ in range(10):
+        o.step(np.float32(dt))
+        g.step(float(np.float32(dt)))
+    err = state_error(g.get_state(), o.state)
+    assert err[0] <= 1e-4 and err[4] <= 1e-4, err
+
+
+def test_nonphysical_state_is_reported(port):
+    """test_kernels.cpp:279-288 + error.hpp payload: poisoned density."""
+    o, g = make(port, "unit", (1,), 2, gravity=0.0)
+    q = o.init_case(po.CASE_CONSTANT, 0, [1.0, 0.0, 0.0, 0.0, 1e5]).copy()
+    q[3, 0, 5] = -1.0
+    with pytest.raises(capi.NonPhysicalState) as ei:
+        g.assemble_rhs(q)
+    assert ei.value.element == 3 and ei.value.node == 5
+    assert ei.value.rho == -1.0 and ei.value.pressure == 0.0
+    with pytest.raises(po.NonPhysicalState) as eo:
+        o.assemble_rhs(q)
+    assert (eo.value.element, eo.value.node) == (3, 5)
+    # the flag is cleared: a clean state passes again
+    q[3, 0, 5] = 1.0
+    g.assemble_rhs(q)
+
+
+def test_nonphysical_stage_in_step(port):
+    """solver.hpp:141-143: the stage of the failing RHS is attached."""
+    o, g = make(port, "unit", (1,), 2, gravity=0.0)
+    q = o.init_case(po.CASE_CONSTANT, 0, [1.0, 0.0, 0.0, 0.0, 1e5]).copy()
+    q[1, 4, 2] = -5.0   # negative energy -> negative pressure in stage 0
+    g.set_state(q)
+    with pytest.raises(capi.NonPhysicalState) as ei:
+        g.step(1e-3)
+    assert ei.value.stage == 0 and ei.value.element == 1 and ei.value.node == 2
+
+
+def test_init_case_matches_oracle(port):
+    for case, seed in ((po.CASE_BUBBLE_SHARP, 0), (po.CASE_BUBBLE_SMOOTH, 0), (po.CASE_HYDROSTATIC, 0),
+                       (po.CASE_ENTROPY_TEST, 77)):
+        for prec in ("f64", "f32"):
+            o, g = make(port, "bubble", (1, False), 4, prec=prec)
+            q = o.init_case(case, seed)
+            g.init_case(case, seed)
+            assert np.array_equal(g.get_state(), q)
+            assert np.array_equal(g.get_phi(), o.phi)
+
+
+def test_diagnostics_match_oracle(port):
+    o, g = make(port, "bubble", (1, False), 4)
+    q = o.init_case(po.CASE_BUBBLE_SMOOTH).copy()
+    g.set_state(q)
+    for var in (0, 4):
+        assert g.quadrature_total(var) == o.quadrature_total(q, var)
+    assert g.total_entropy() == o.total_entropy(q)
+    g.rhs(0.0, 1.0)
+    k = g.get_state(capi.REG_K)
+    assert g.entropy_production() == o.entropy_production(q, k)
+
+
+def test_axpy_and_lsrk_pieces(port):
+    o, g = make(port, "bubble", (1, True), 3)
+    rng = np.random.default_rng(0)
+    q = rng.standard_normal(g.shape)
+    k = rng.standard_normal(g.shape)
+    g.set_state(q, capi.REG_Q)
+    g.set_state(k, capi.REG_K)
+    g.axpy(0.37)
+    assert np.array_equal(g.get_state(), q + 0.37 * k)
