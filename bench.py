@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the ESDG right-hand side + LSRK update on B200.
+
+    python bench.py --gpus N --steps K --warmup W          (our arm)
+    python bench.py --impl reference --gpus N --steps K --warmup W
+
+A "step" is one five-stage LSRK step (5 RHS evaluations + 5 updates) of the
+rising-thermal-bubble case (BASELINE.json configs[1]: N=4, ~1e8 DOF per GPU,
+FP64). metric = RHS DOF-updates/s = elements * (N+1)^3 * RHS evaluations / s,
+whole job. For N > 1 the driver launches this file under torchrun, one rank
+per GPU; the mesh grows with N (configs[4], weak scaling) and the face-trace
+halo moves over NCCL while the volume kernel runs.
+
+Prints ONE JSON line on rank 0. See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rhs_dof_updates_per_s"
+UNIT = "DOF-updates/s"
+
+# configs[4] of BASELINE.json: base lattice per GPU count at refinement 5
+WEAK_BASE = {1: (3, 3, 3), 2: (6, 3, 3), 4: (6, 6, 3), 8: (6, 6, 6)}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--order", type=int, default=4)
+    ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--path", default="fused", choices=["fused", "split"])
+    ap.add_argument("--refinement", type=int, default=5)
+    ap.add_argument("--base", type=int, nargs=3, default=None,
+                    help="override the base lattice (default: configs[4] table)")
+    ap.add_argument("--case", default="bubble", choices=["bubble", "baroclinic"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------
+# clocks: sampled with nvidia-smi DURING the timed region
+# --------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) < 7:
+                continue
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, r[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# --------------------------------------------------------------------------
+# algorithmic work per element per RHS (the
+# reference's own PerfRecord model, diagnostics.cpp:33-81)
+# --------------------------------------------------------------------------
+def work_model(nq: int, bytes_per_real: int):
+    n2, n3, h = nq * nq, nq ** 3, nq // 2
+    return {
+        "volume_flops": n3 * (189 * h + 205),
+        "volume_bytes": (11 * n3 + n2) * bytes_per_real,
+        "surface_flops": 843 * n2,
+        "surface_bytes": 66 * n2 * bytes_per_real,
+        "update_bytes": 15 * n3 * bytes_per_real,
+    }
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f), "MEASURED_PEAKS.json"
+    return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes per launch from the committed ncu summary, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f).get(kernel)
+    return None
+
+
+# --------------------------------------------------------------------------
+# CPU arm: the reference's own Solver<Real> (oracle/_ref) or the oracle port
+# --------------------------------------------------------------------------
+def cpu_has_avx2_fma() -> bool:
+    try:
+        with open("/proc/cpuinfo") as f:
+            flags = next((l for l in f if l.startswith("flags")), "")
+        return " avx2 " in flags + " " and " fma " in flags + " "
+    except OSError:
+        return False
+
+
+def run_cpu_reference(order, precision, target_seconds, steps=None, warmup=1):
+    """Times Solver::step on a bounded sample of the bench workload: the same
+    bubble case, same order and precision, on a 16^3-element box (the
+    reference cannot hold 1e8 DOF: 17 Reals of flux record per face node)."""
+    from oracle import pyoracle as po
+    threads = os.cpu_count() or 1
+    if po.reference_available():
+        fast = po.reference_available(fast=True) and cpu_has_avx2_fma()
+        ora, kind = po.Oracle("reference", fast=fast), "reference"
+        build = "-O3 -march=x86-64-v3" if fast else "-O2"
+    else:
+        ora, kind, build, threads = po.Oracle("port"), "port", "-O2 (C restatement, serial)", 1
+    refinement = 4
+    mesh = ora.mesh(po.bubble_mesh_config(refinement))
+    ranks = max(1, min(threads, mesh.ne))
+    solver = mesh.solver(order, precision, ranks=ranks) if kind == "reference" else mesh.solver(order, precision)
+    solver.init_case(po.CASE_BUBBLE_SHARP)
+    dt = solver.compute_dt(0.5)
+    dof = mesh.ne * solver.n3
+    for _ in range(max(1, warmup)):
+        t0 = time.perf_counter()
+        solver.step(dt)
+        one = time.perf_counter() - t0
+    if steps is None:
+        steps = int(max(2, min(200, target_seconds / max(one, 1e-6))))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        solver.step(dt)
+    wall = time.perf_counter() - t0
+    value = dof * 5 * steps / wall
+    return {
+        "value": value, "unit": UNIT, "cores": ranks if kind == "reference" else 1, "kind": kind,
+        "sample": (f"bubble N={order} {precision} on {mesh.ne} elements ({dof} DOF), {steps} LSRK steps, "
+                   f"Solver<Real>::step with ranks={ranks} worker threads, built {build}"),
+        "ms_per_step": 1e3 * wall / steps, "steps": steps,
+    }
+
+
+def main_reference(args, rank):
+    if rank != 0:
+        return
+    res = run_cpu_reference(args.order, args.precision, args.cpu_seconds,
+                            steps=args.steps, warmup=args.warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+        "config": {"workload": f"rising thermal bubble, N={args.order}, {args.precision}: "
+                               "bounded CPU sample of BASELINE.json configs[1]",
+                   "sample": res["sample"]},
+        "cpu_baseline": {"value": res["value"], "unit": UNIT, "cores": res["cores"],
+                         "kind": res["kind"], "sample": res["sample"]},
+        "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+def main_b200(args, rank, local_rank, world):
+    import torch
+    from paper_2605_16684_b200 import capi
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    device = local_rank
+    torch.cuda.set_device(device)
+
+    nq = args.order + 1
+    rb = 8 if args.precision == "f64" else 4
+    base = tuple(args.base) if args.base else WEAK_BASE.get(world, (3 * world, 3, 3))
+    if args.case == "bubble":
+        scale = tuple(b / 3.0 for b in base) if not args.base else (1, 1, 1)
+        cfg = capi.bubble_mesh_config(args.refinement, False, base, scale)
+        settings = capi.Settings(1, 0, 0.0, 0.0, 0.0)
+        case_id = capi.CASE_BUBBLE_SHARP
+    else:
+        base = tuple(args.base) if args.base else (12, 2 * world, 1)
+        cfg = capi.channel_mesh_config(args.refinement, base)
+        settings = capi.Settings(1, 2, 1e-4, 1.6e-11, 3e6)
+        case_id = capi.CASE_BAROCLINIC
+    mesh = capi.Mesh(cfg)
+
+    if world > 1:
+        from paper_2605_16684_b200 import halo
+        solver = capi.GpuSolver(mesh, args.order, args.precision, settings=settings,
+                                distributed=(world, rank, device))
+        cb, exchange = halo.make_exchange_callback(solver, device)
+        solver.exchange_impl = cb
+    else:
+        solver = capi.GpuSolver(mesh, args.order, args.precision, settings=settings, devices=[device])
+        exchange = None
+    solver.set_path(capi.PATH_FUSED if args.path == "fused" else capi.PATH_SPLIT)
+    solver.init_case(case_id)
+    dt_local = solver.compute_dt(0.5)
+    if world > 1:
+        t = torch.tensor([dt_local], dtype=torch.float64, device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        dt_local = float(t.item())
+    dt = dt_local
+    n_local = solver.end - solver.begin
+    dof_total = mesh.ne * solver.n3
+
+    stream = torch.cuda.ExternalStream(solver.stream, device=device)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(device)
+
+    # ---- warm-up ----------------------------------------------------------
+    for _ in range(max(args.warmup, 3)):
+        solver.step(dt, check_state=True)
+    solver.sync()
+
+    # ---- timed region: exactly K steps, device events, max over ranks -----
+    solver.enable_timing(True)
+    solver.timers(reset=True)
+    launches0 = solver.timers()["launches"]
+    sampler = ClockSampler(device)
+    if rank == 0:
+        sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        solver.step(dt, check_state=False)
+    e1.record(stream)
+    solver.sync()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    clocks = sampler.stop() if rank == 0 else None
+    timers = solver.timers(reset=True)
+    solver.enable_timing(False)
+    solver.step(dt, check_state=True)   # the state is still physical
+    solver.sync()
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    n_rhs = 5 * args.steps
+    value = dof_total * n_rhs / (ms * 1e-3)
+
+    # ---- e2e: host buffers in, host buffers out, copies inside the region --
+    e2e = None
+    if not args.no_e2e:
+        torch_dtype = torch.float64 if rb == 8 else torch.float32
+        host_q = torch.empty((n_local, 5, solver.n3), dtype=torch_dtype, pin_memory=True)
+        nbytes = host_q.numel() * host_q.element_size()
+        L = capi.lib()
+        capi.check(L.esdg_b200_solver_get_state(solver.h, capi.REG_Q, host_q.data_ptr()))
+        e2e_steps = max(2, min(args.steps, 4))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            capi.check(L.esdg_b200_solver_set_state(solver.h, capi.REG_Q, host_q.data_ptr()))
+            solver.step(dt, check_state=True)
+            capi.check(L.esdg_b200_solver_get_state(solver.h, capi.REG_Q, host_q.data_ptr()))
+        barrier()
+        wall = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([wall], dtype=torch.float64, device=f"cuda:{device}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            wall = float(t.item())
+        e2e = {"value": dof_total * 5 * e2e_steps / wall, "unit": UNIT,
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "steps": e2e_steps,
+               "call": "esdg_b200_solver_set_state + esdg_b200_solver_step + "
+                       "esdg_b200_solver_get_state on pinned host StateField buffers"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel -----------------------------------
+    peaks, peak_src = measured_peaks()
+    fma_peak = capi.measure_fma_peak(device, rb)
+    w = work_model(nq, rb)
+    per_launch = {k: timers[k] / n_rhs for k in ("volume", "surface", "update")}
+    kernels = {}
+    if args.path == "fused":
+        flops = (w["volume_flops"] + w["surface_flops"]) * n_local
+        dom = "rhs_kernel<VOL,SURF> (fused K1+K2)"
+        dom_s = per_launch["volume"]
+    else:
+        flops = w["volume_flops"] * n_local
+        dom = "rhs_kernel<VOL> (K1 volume)"
+        dom_s = per_launch["volume"]
+        surf_gbs = w["surface_bytes"] * n_local / per_launch["surface"] / 1e9
+        kernels["surface"] = {"bound": "hbm", "achieved": surf_gbs, "peak": peaks["hbm_gbs"],
+                              "unit": "GB/s", "frac": surf_gbs / peaks["hbm_gbs"],
+                              "ms": 1e3 * per_launch["surface"]}
+    achieved = flops / dom_s / 1e12
+    upd_gbs = w["update_bytes"] * n_local / per_launch["update"] / 1e9
+    kernels["update"] = {"bound": "hbm", "achieved": upd_gbs, "peak": peaks["hbm_gbs"],
+                         "unit": "GB/s", "frac": upd_gbs / peaks["hbm_gbs"],
+                         "ms": 1e3 * per_launch["update"]}
+    roofline = {
+        "kernel": dom, "bound": "fp64" if rb == 8 else "fp32",
+        "achieved": achieved, "peak": fma_peak, "unit": "TFLOP/s", "frac": achieved / fma_peak,
+        "traffic": ncu_traffic("fused" if args.path == "fused" else "volume"),
+        "ms_per_launch": 1e3 * dom_s,
+        "flops_model": "reference PerfRecord model (diagnostics.cpp:33-81): "
+                       f"{flops // n_local} flops/element/launch",
+        "peak_source": ("CUDA-core FMA peak measured in this run by esdg_b200_measure_fma_peak "
+                        f"(register-operand FMA chains); HBM peak from {peak_src}"),
+        "other_kernels": kernels,
+    }
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            cpu = run_cpu_reference(args.order, args.precision, args.cpu_seconds)
+            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as exc:  # the baseline must never sink the bench line
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
+                   "sample": f"unavailable: {exc!r}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": args.precision, "data": "synthetic",
+        "config": {
+            "workload": (f"{'rising thermal bubble' if args.case == 'bubble' else 'baroclinic channel'}"
+                         f", N={args.order}, {mesh.ne} hex elements, {dof_total} DOF, {args.precision}"
+                         f" (BASELINE.json configs[{'1' if world == 1 else '4'}])"),
+            "elements": mesh.ne, "dof": dof_total, "order": args.order,
+            "base": list(base), "refinement": args.refinement, "path": args.path,
+            "rhs_per_step": 5, "dt": dt, "partition": f"morton x{world}",
+            "l2": "inputs_exceed_l2 (state registers are GBs; 126 MB L2)",
+        },
+        "clocks": clocks, "e2e": e2e, "gpu_launches": timers["launches"] - launches0,
+        "roofline": roofline, "cpu_baseline": cpu,
+    }
+    if exchange is not None:
+        line["config"]["halo_exchanges"] = exchange.exchanges
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        main_reference(args, rank)
+        return
+    main_b200(args, rank, local_rank, world)
+
+
+if __name__ == "__main__":
+    main()

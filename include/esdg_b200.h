@@ -214,6 +214,20 @@ int esdg_b200_partition(int64_t n_elements, int ranks, int64_t* range_begin);
 int esdg_b200_exchange_plan(esdg_b200_mesh* m, int ranks, int32_t* ghost_count,
                             int32_t* interior_count,
                             esdg_b200_ghost_face* ghosts, int32_t* interior);
+/* Host-only: the GPU-side slice of the exchange for partition `rank` of
+ * `world_size`, i.e. exactly what esdg_b200_shard_create consumes. Ghost
+ * faces are ordered by (peer, face) so that one contiguous block of traces
+ * moves per peer and both ends enumerate a block identically. Call with the
+ * array arguments NULL to obtain *n_peers and *n_ghost first.
+ *   peer/offset/count [n_peers]: block of peer p is traces
+ *                                [offset, offset+count) of BOTH the send and
+ *                                the receive buffer of this rank
+ *   send_elem/send_face [n_ghost]: local element and local face of slot g
+ *   nbr_local [(end-begin)*6]: neighbour codes as in esdg_b200_shard_desc */
+int esdg_b200_rank_halo(esdg_b200_mesh* m, int world_size, int rank,
+                        int32_t* n_peers, int64_t* n_ghost, int32_t* peer,
+                        int64_t* offset, int64_t* count, int32_t* send_elem,
+                        int32_t* send_face, int32_t* nbr_local);
 /* LsrkScheme (time_integration.hpp:17-37) */
 void esdg_b200_lsrk_coefficients(double a[5], double b[5], double c[5]);
 
@@ -281,6 +295,8 @@ int esdg_b200_solver_n3(const esdg_b200_solver* s);
  * 5*nq^2 Reals) belong to rank peer[p]. Returns n_peers. */
 int esdg_b200_solver_halo(const esdg_b200_solver* s, int32_t* peer,
                           int64_t* offset, int64_t* count, int capacity);
+/* compute stream of the (single) local partition, as cudaStream_t */
+void* esdg_b200_solver_stream(esdg_b200_solver* s);
 void* esdg_b200_solver_send_ptr(esdg_b200_solver* s);
 void* esdg_b200_solver_recv_ptr(esdg_b200_solver* s);
 int64_t esdg_b200_solver_n_ghost(const esdg_b200_solver* s);

@@ -107,6 +107,7 @@ SIGNATURES = {
     "esdg_b200_reference_element": (_i, [_i, _dp, _dp, _dp]),
     "esdg_b200_partition": (_i, [_i64, _i, _i64p]),
     "esdg_b200_exchange_plan": (_i, [_vp, _i, _ip, _ip, C.POINTER(GhostFace), _ip]),
+    "esdg_b200_rank_halo": (_i, [_vp, _i, _i, _ip, _i64p, _ip, _i64p, _i64p, _ip, _ip, _ip]),
     "esdg_b200_lsrk_coefficients": (None, [_dp, _dp, _dp]),
     "esdg_b200_solver_create": (_i, [_vp, _i, C.POINTER(Gas), C.POINTER(Settings), _i, _i,
                                      _ip, _i, C.POINTER(_vp)]),
@@ -120,6 +121,7 @@ SIGNATURES = {
     "esdg_b200_solver_local_end": (_i64, [_vp]),
     "esdg_b200_solver_n3": (_i, [_vp]),
     "esdg_b200_solver_halo": (_i, [_vp, _ip, _i64p, _i64p, _i]),
+    "esdg_b200_solver_stream": (_vp, [_vp]),
     "esdg_b200_solver_send_ptr": (_vp, [_vp]),
     "esdg_b200_solver_recv_ptr": (_vp, [_vp]),
     "esdg_b200_solver_n_ghost": (_i64, [_vp]),
@@ -275,6 +277,29 @@ class Mesh:
                     interior=interior[:int(ic.sum())].copy())
 
 
+def rank_halo(mesh: Mesh, world_size: int, rank: int):
+    """GPU-side halo lists of one partition (host only, no device needed)."""
+    npeers, nghost = C.c_int32(), C.c_int64()
+    check(lib().esdg_b200_rank_halo(mesh.h, world_size, rank, C.byref(npeers), C.byref(nghost),
+                                    None, None, None, None, None, None))
+    rb = partition(mesh.ne, world_size)
+    nloc = int(rb[rank + 1] - rb[rank])
+    peer = np.zeros(max(1, npeers.value), np.int32)
+    off = np.zeros(max(1, npeers.value), np.int64)
+    cnt = np.zeros(max(1, npeers.value), np.int64)
+    se = np.zeros(max(1, nghost.value), np.int32)
+    sf = np.zeros(max(1, nghost.value), np.int32)
+    nbr = np.zeros((nloc, 6), np.int32)
+    check(lib().esdg_b200_rank_halo(mesh.h, world_size, rank, C.byref(npeers), C.byref(nghost),
+                                    peer.ctypes.data_as(_ip), off.ctypes.data_as(_i64p),
+                                    cnt.ctypes.data_as(_i64p), se.ctypes.data_as(_ip),
+                                    sf.ctypes.data_as(_ip), nbr.ctypes.data_as(_ip)))
+    n, g = npeers.value, nghost.value
+    return dict(begin=int(rb[rank]), end=int(rb[rank + 1]),
+                peers=[(int(peer[i]), int(off[i]), int(cnt[i])) for i in range(n)],
+                send_elem=se[:g].copy(), send_face=sf[:g].copy(), nbr_local=nbr)
+
+
 def reference_element(order):
     nq = order + 1
     x, w, d = np.zeros(nq), np.zeros(nq), np.zeros(nq * nq)
@@ -312,8 +337,17 @@ class GpuSolver:
                                                 self.prec, ranks, dev.ctypes.data_as(_ip), dev.size,
                                                 C.byref(h)))
         else:
-            world, rank, device, fn = distributed
-            self._cb = EXCHANGE_FN(fn) if fn is not None else EXCHANGE_FN(0)
+            world, rank, device = distributed
+            # late-bound trampoline: the exchange needs the solver's buffers,
+            # which only exist after creation (see halo.make_exchange_callback)
+            self.exchange_impl = None
+
+            def _trampoline(user, phase, stream):
+                if self.exchange_impl is None:
+                    return 1
+                return self.exchange_impl(user, phase, stream)
+
+            self._cb = EXCHANGE_FN(_trampoline)
             check(lib().esdg_b200_solver_create_distributed(
                 mesh.h, order, C.byref(self.gas), C.byref(self.settings), self.prec, world, rank,
                 device, self._cb, None, C.byref(h)))
@@ -415,6 +449,20 @@ class GpuSolver:
         n = C.c_int64()
         self._chk(lib().esdg_b200_solver_timers(self.h, s.ctypes.data_as(_dp), C.byref(n), int(reset)))
         return dict(volume=s[0], surface=s[1], update=s[2], pack=s[3], launches=n.value)
+
+    @property
+    def stream(self) -> int:
+        return int(lib().esdg_b200_solver_stream(self.h) or 0)
+
+    @property
+    def n_ghost(self) -> int:
+        return int(lib().esdg_b200_solver_n_ghost(self.h))
+
+    def halo_buffers(self):
+        """(send_ptr, recv_ptr, bytes per trace) of a single-partition solver."""
+        return (int(lib().esdg_b200_solver_send_ptr(self.h) or 0),
+                int(lib().esdg_b200_solver_recv_ptr(self.h) or 0),
+                self.prec * 5 * self.nq * self.nq)
 
     def halo(self):
         cap = 64

@@ -130,6 +130,27 @@ int esdg_b200_exchange_plan(esdg_b200_mesh* m, int ranks, int32_t* ghost_count,
   return 2 * n_pairs;
 }
 
+int esdg_b200_rank_halo(esdg_b200_mesh* m, int world_size, int rank, int32_t* n_peers,
+                        int64_t* n_ghost, int32_t* peer, int64_t* offset, int64_t* count,
+                        int32_t* send_elem, int32_t* send_face, int32_t* nbr_local) {
+  if (!m || !n_peers || !n_ghost || rank < 0 || rank >= world_size) return ESDG_B200_BADARG;
+  std::vector<int64_t> rb;
+  if (!esdg_b200::host::make_partition(m->m->ne, world_size, rb)) return ESDG_B200_BADARG;
+  esdg_b200::host::RankHalo h;
+  esdg_b200::host::build_rank_halo(*m->m, rb, rank, h);
+  *n_peers = int32_t(h.peers.size());
+  *n_ghost = int64_t(h.send_elem.size());
+  for (size_t i = 0; i < h.peers.size(); ++i) {
+    if (peer) peer[i] = h.peers[i].rank;
+    if (offset) offset[i] = h.peers[i].offset;
+    if (count) count[i] = h.peers[i].count;
+  }
+  if (send_elem) std::memcpy(send_elem, h.send_elem.data(), sizeof(int32_t) * h.send_elem.size());
+  if (send_face) std::memcpy(send_face, h.send_face.data(), sizeof(int32_t) * h.send_face.size());
+  if (nbr_local) std::memcpy(nbr_local, h.nbr_local.data(), sizeof(int32_t) * h.nbr_local.size());
+  return ESDG_B200_OK;
+}
+
 void esdg_b200_lsrk_coefficients(double a[5], double b[5], double c[5]) {
   esdg_b200::host::lsrk_coefficients(a, b, c);
 }
@@ -207,6 +228,9 @@ int esdg_b200_solver_n3(const esdg_b200_solver* s) { return s ? s->core->n3() : 
 int esdg_b200_solver_halo(const esdg_b200_solver* s, int32_t* peer, int64_t* offset,
                           int64_t* count, int capacity) {
   return s ? s->core->halo(peer, offset, count, capacity) : 0;
+}
+void* esdg_b200_solver_stream(esdg_b200_solver* s) {
+  return (s && s->core->n_shards() >= 1) ? s->core->shard(0)->stream() : nullptr;
 }
 void* esdg_b200_solver_send_ptr(esdg_b200_solver* s) {
   return (s && s->core->n_shards() == 1) ? s->core->shard(0)->send_ptr() : nullptr;

@@ -1,0 +1,153 @@
+"""Host-side logic of the product (mesh, operators, partition, exchange plan,
+GPU halo lists) against the oracle, and the C-ABI surface: the library loads
+without a GPU and exports every symbol include/esdg_b200.h declares. No
+compute entry point is called here. CPU only."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+from paper_2605_16684_b200 import capi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+MESHES = [
+    (po.bubble_mesh_config(3), capi.bubble_mesh_config(3)),
+    (po.bubble_mesh_config(1, True), capi.bubble_mesh_config(1, True)),
+    (po.mesh_config((3, 1, 2), 1, (0., 0., 0.), (3., 1., 2.), (0, 1, 0)),
+     capi.mesh_config((3, 1, 2), 1, (0., 0., 0.), (3., 1., 2.), (0, 1, 0))),
+    (po.mesh_config((1, 1, 1), 0), capi.mesh_config((1, 1, 1), 0)),
+    (po.mesh_config((5, 3, 2), 0, bc=(1, 1, 1)), capi.mesh_config((5, 3, 2), 0, bc=(1, 1, 1))),
+    (po.mesh_config((12, 2, 1), 1, (0., 0., 0.), (4e7, 6e6, 3e4), (0, 1, 1)), capi.channel_mesh_config(1)),
+]
+
+
+def test_header_symbols_exported_and_bound():
+    """Every function include/esdg_b200.h declares is exported by the shared
+    library and has a ctypes signature (so the binding cannot drift)."""
+    text = open(os.path.join(ROOT, "include", "esdg_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    declared = set(re.findall(r"\b(esdg_b200_[a-z0-9_]+)\s*\(", text))
+    declared -= {"esdg_b200_exchange_fn"}
+    assert len(declared) > 50
+    lib = capi.lib()
+    for name in sorted(declared):
+        assert hasattr(lib, name), f"{name} not exported"
+        assert name in capi.SIGNATURES, f"{name} has no ctypes signature"
+    assert set(capi.SIGNATURES) <= declared
+    assert lib.esdg_b200_abi_version() == 1
+
+
+def test_no_silent_cpu_fallback():
+    """Without a device every compute path must fail loudly."""
+    if capi.lib().esdg_b200_device_count() > 0:
+        pytest.skip("a GPU is present")
+    mesh = capi.Mesh(capi.bubble_mesh_config(1))
+    with pytest.raises(capi.EsdgError):
+        capi.GpuSolver(mesh, 4, "f64")
+    with pytest.raises(capi.EsdgError):
+        capi.measure_fma_peak(0, 8)
+
+
+def test_product_never_imports_oracle():
+    """oracle/ is test infrastructure: nothing under the package references it."""
+    pkg = os.path.join(ROOT, "paper_2605_16684_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".hpp", ".h")) or f == "Makefile":
+                src = open(os.path.join(dirpath, f), errors="ignore").read()
+                assert "pyoracle" not in src and "liboracle" not in src and "esdg_oracle" not in src, f
+                assert "libesdg_ref" not in src, f
+
+
+def test_operators_and_lsrk(port):
+    for order in range(1, 8):
+        for a, b in zip(port.reference_element(order), capi.reference_element(order)):
+            assert np.array_equal(a, b)
+    for a, b in zip(port.lsrk(), capi.lsrk_coefficients()):
+        assert np.array_equal(a, b)
+    with pytest.raises(capi.EsdgError):
+        capi.reference_element(0)
+
+
+@pytest.mark.parametrize("idx", range(len(MESHES)))
+def test_mesh_and_plan_match_oracle(port, idx):
+    oc, cc = MESHES[idx]
+    mo, mc = port.mesh(oc), capi.Mesh(cc)
+    assert (mo.ne, mo.nfaces) == (mc.ne, mc.nfaces)
+    assert np.array_equal(mo.lattice, mc.lattice)
+    assert np.array_equal(mo.faces, mc.faces)
+    assert np.array_equal(mo.face_of, mc.face_of)
+    # neighbour table is consistent with the face list
+    nbr, faces, face_of = mc.neighbors, mc.faces, mc.face_of
+    for e in range(mc.ne):
+        for lf in range(6):
+            me, pe, d, ms, refl = faces[face_of[e, lf]]
+            assert d == lf // 2
+            if refl:
+                assert nbr[e, lf] == -1
+            else:
+                assert nbr[e, lf] == (pe if (me == e and ms == lf % 2) else me)
+    for ranks in (1, 2, 3, 4, 8):
+        if ranks > mo.ne:
+            with pytest.raises(capi.EsdgError):
+                capi.partition(mo.ne, ranks)
+            continue
+        assert np.array_equal(port.partition(mo.ne, ranks), capi.partition(mo.ne, ranks))
+        a, b = mo.exchange_plan(ranks), mc.exchange_plan(ranks)
+        for k in a:
+            assert np.array_equal(a[k], b[k]), (k, ranks)
+
+
+def test_mesh_rejects_bad_config():
+    for cfg in (capi.mesh_config((0, 1, 1)), capi.mesh_config(refinement=-1), capi.mesh_config(refinement=21),
+                capi.mesh_config(lo=(0, 0, 0), hi=(1, 0, 1))):
+        with pytest.raises(capi.EsdgError):
+            capi.Mesh(cfg)
+
+
+@pytest.mark.parametrize("idx", [0, 1, 2, 5])
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_rank_halo_consistency(port, idx, world):
+    """The GPU halo lists: every ghost face of rank A toward B appears in B's
+    block toward A at the same position, pointing at the opposite side of the
+    same face; local codes address the right elements."""
+    oc, cc = MESHES[idx]
+    mo, mc = port.mesh(oc), capi.Mesh(cc)
+    if world > mc.ne:
+        pytest.skip("more ranks than elements")
+    face_of, faces, nbr = mo.face_of, mo.faces, mc.neighbors
+    halos = [capi.rank_halo(mc, world, r) for r in range(world)]
+    plan = mo.exchange_plan(world)
+    assert [len(h["send_elem"]) for h in halos] == list(plan["ghost_count"])
+    for r, h in enumerate(halos):
+        b, e = h["begin"], h["end"]
+        codes = h["nbr_local"]
+        seen = set()
+        for el in range(e - b):
+            for lf in range(6):
+                n, code = nbr[b + el, lf], codes[el, lf]
+                if n < 0:
+                    assert code == -1
+                elif b <= n < e:
+                    assert code == n - b
+                else:
+                    v = -2 - code
+                    slot, am_minus = v >> 1, v & 1
+                    assert h["send_elem"][slot] == el and h["send_face"][slot] == lf
+                    me, pe, d, ms, refl = faces[face_of[b + el, lf]]
+                    assert am_minus == int(me == b + el and ms == lf % 2)
+                    seen.add(slot)
+        assert seen == set(range(len(h["send_elem"])))
+        assert sum(c for _, _, c in h["peers"]) == len(h["send_elem"])
+        for peer, off, cnt in h["peers"]:
+            hp = halos[peer]
+            poff = [o for (p, o, c) in hp["peers"] if p == r]
+            assert len(poff) == 1 and [c for (p, o, c) in hp["peers"] if p == r] == [cnt]
+            for i in range(cnt):
+                mine = face_of[b + h["send_elem"][off + i], h["send_face"][off + i]]
+                theirs = face_of[hp["begin"] + hp["send_elem"][poff[0] + i], hp["send_face"][poff[0] + i]]
+                assert mine == theirs
+                assert h["send_face"][off + i] == hp["send_face"][poff[0] + i] ^ 1
