@@ -143,6 +143,7 @@ SIGNATURES = {
     "esdg_b200_solver_enable_timing": (_i, [_vp, _i]),
     "esdg_b200_solver_timers": (_i, [_vp, _dp, _i64p, _i]),
     "esdg_b200_measure_fma_peak": (_i, [_i, _i, _dp]),
+    "esdg_b200_selftest": (_i, [_i, _i, _dp]),
 }
 
 
@@ -470,6 +471,13 @@ class GpuSolver:
         n = lib().esdg_b200_solver_halo(self.h, peer.ctypes.data_as(_ip), off.ctypes.data_as(_i64p),
                                         cnt.ctypes.data_as(_i64p), cap)
         return [(int(peer[i]), int(off[i]), int(cnt[i])) for i in range(n)]
+
+
+def selftest(device=0, precision=8):
+    out = np.zeros(4)
+    check(lib().esdg_b200_selftest(device, precision, out.ctypes.data_as(_dp)))
+    return dict(rcp_max_ulp=out[0], rcp_scaling_violations=int(out[1]), rcp_one_exact=bool(out[2]),
+                samples=int(out[3]))
 
 
 def measure_fma_peak(device=0, precision=8) -> float:

@@ -10,10 +10,11 @@ namespace {
 template <class Real, int NQ, bool VOL, bool SURF>
 cudaError_t launch_one(const dev::RhsParams<Real, NQ>& P, cudaStream_t stream) {
   constexpr int EPB = dev::Tile<NQ, sizeof(Real)>::EPB;
+  constexpr int MINB = dev::Tile<NQ, sizeof(Real)>::MINB;
   constexpr int T = EPB * NQ * NQ;
   constexpr size_t smem =
       size_t(dev::V_COUNT + 5) * EPB * dev::Geo<NQ>::N3P * sizeof(Real);
-  auto kern = dev::rhs_kernel<Real, NQ, EPB, VOL, SURF>;
+  auto kern = dev::rhs_kernel<Real, NQ, EPB, MINB, VOL, SURF>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {

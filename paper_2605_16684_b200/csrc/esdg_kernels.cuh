@@ -35,6 +35,8 @@
 namespace esdg_b200 {
 namespace dev {
 
+struct FlagRecord;
+
 template <class Real, int NQ>
 struct RhsParams {
   const Real* q;
@@ -46,6 +48,7 @@ struct RhsParams {
   const int32_t* ylevel;
   const Real* cor_f;
   unsigned long long* flag;
+  FlagRecord* flag_records;
   long long ne;
   long long elem_offset;
   Real a_old, a_new;
@@ -57,15 +60,38 @@ struct RhsParams {
   int stage;
 };
 
-// Non-physical-state key: smallest (stage, element, node) wins, which is the
-// state the reference's serial sweep would have thrown on first.
-__device__ __forceinline__ void raise_flag(unsigned long long* flag, int stage,
-                                           long long elem, int node) {
+// Non-physical-state record. The smallest key wins:
+//   [stage:8][phase:1][element:45][node:10]
+// phase 0 = the per-node sweep of phase A (the reference's volume phase,
+// which runs first and throws first, solver.hpp:259-262), phase 1 = a
+// neighbour state met while evaluating a face. Within a phase the smallest
+// (element, node) is what the reference's serial sweep would have hit first.
+// The payload (rho, p) goes to a small hashed side table so the host can
+// report the values seen at detection time even after later stages ran.
+struct FlagRecord {
+  unsigned long long key;
+  double rho, p;
+};
+constexpr int kFlagSlots = 61;
+
+__device__ __forceinline__ void raise_flag(unsigned long long* flag,
+                                           FlagRecord* records, int stage,
+                                           int phase, long long elem, int node,
+                                           double rho, double p) {
   const unsigned long long key =
       (static_cast<unsigned long long>(stage < 0 ? 0 : stage) << 56) |
+      (static_cast<unsigned long long>(phase) << 55) |
       (static_cast<unsigned long long>(elem) << 10) |
       static_cast<unsigned long long>(node);
-  atomicMin(flag, key);
+  const unsigned long long old = atomicMin(flag, key);
+  if (key < old) {
+    FlagRecord* r = records + (key % kFlagSlots);
+    r->rho = rho;
+    // compute_node_vals reports p = 0 when the density check trips first
+    r->p = (rho > 0.0) ? p : 0.0;
+    __threadfence();
+    r->key = key;
+  }
 }
 
 template <int NQ>
@@ -86,15 +112,15 @@ __device__ __forceinline__ Node<Real> load_node(const Real* vals, int VS, int s,
   Node<Real> n;
   const int d1 = dir == 2 ? 0 : dir + 1;
   const int d2 = d1 == 2 ? 0 : d1 + 1;
-  n.rho = vals[V_RHO * VS + s];
+  n.hr = vals[V_HR * VS + s];
   n.hun = vals[(V_HU0 + dir) * VS + s];
   n.hut1 = vals[(V_HU0 + d1) * VS + s];
   n.hut2 = vals[(V_HU0 + d2) * VS + s];
   n.b = vals[V_B * VS + s];
-  n.lr = vals[V_LR * VS + s];
+  n.hlr = vals[V_HLR * VS + s];
   n.lb = vals[V_LB * VS + s];
   n.hphi = vals[V_HPHI * VS + s];
-  n.ib = vals[V_IB * VS + s];
+  n.hib = vals[V_HIB * VS + s];
   return n;
 }
 
@@ -104,20 +130,20 @@ __device__ __forceinline__ Node<Real> rotate_node(const Real nv[V_COUNT],
   Node<Real> n;
   const int d1 = dir == 2 ? 0 : dir + 1;
   const int d2 = d1 == 2 ? 0 : d1 + 1;
-  n.rho = nv[V_RHO];
+  n.hr = nv[V_HR];
   n.hun = dir == 0 ? nv[V_HU0] : (dir == 1 ? nv[V_HU1] : nv[V_HU2]);
   n.hut1 = d1 == 0 ? nv[V_HU0] : (d1 == 1 ? nv[V_HU1] : nv[V_HU2]);
   n.hut2 = d2 == 0 ? nv[V_HU0] : (d2 == 1 ? nv[V_HU1] : nv[V_HU2]);
   n.b = nv[V_B];
-  n.lr = nv[V_LR];
+  n.hlr = nv[V_HLR];
   n.lb = nv[V_LB];
   n.hphi = nv[V_HPHI];
-  n.ib = nv[V_IB];
+  n.hib = nv[V_HIB];
   return n;
 }
 
-template <class Real, int NQ, int EPB, bool VOL, bool SURF>
-__global__ void __launch_bounds__(EPB* NQ* NQ)
+template <class Real, int NQ, int EPB, int MINB, bool VOL, bool SURF>
+__global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     rhs_kernel(const __grid_constant__ RhsParams<Real, NQ> P) {
   using G = Geo<NQ>;
   constexpr int N2 = G::N2, N3 = G::N3, PX = G::PX, N3P = G::N3P;
@@ -143,7 +169,8 @@ __global__ void __launch_bounds__(EPB* NQ* NQ)
     const Real ph = P.phi[(e0 + e) * N3 + n];
     Real nv[V_COUNT], pr;
     if (!node_vals(qv, ph, P.gas.gm1, nv, pr))
-      raise_flag(P.flag, P.stage, P.elem_offset + e0 + e, n);
+      raise_flag(P.flag, P.flag_records, P.stage, 0, P.elem_offset + e0 + e, n,
+                 double(qv[0]), double(pr));
     const int s = e * N3P + G::sidx(n);
 #pragma unroll
     for (int k = 0; k < V_COUNT; ++k) vals[k * VS + s] = nv[k];
@@ -187,11 +214,18 @@ __global__ void __launch_bounds__(EPB* NQ* NQ)
         // diagonal: t_i -= 2 g_d D_ii F(q_i, q_i)  (kernels.hpp:170-188)
 #pragma unroll
         for (int i = 0; i < NQ; ++i) {
-          Real f[5];
-          point_flux(nd[i], P.gas.cg, f);
           const Real cii = P.negc[dir][i * NQ + i];
 #pragma unroll
-          for (int v = 0; v < 5; ++v) acc[i][v] = cii * f[v];
+          for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
+          // D_ii vanishes analytically at interior LGL nodes; the host
+          // flushes its O(1e-16) round-off residue to zero (shard.cu), so
+          // only the two end nodes pay for a point flux here
+          if (cii != Real(0)) {
+            Real f[5];
+            point_flux(nd[i], P.gas.cg, f);
+#pragma unroll
+            for (int v = 0; v < 5; ++v) acc[i][v] = cii * f[v];
+          }
         }
         // off-diagonal pairs, each once (kernels.hpp:190-231)
 #pragma unroll
@@ -202,8 +236,8 @@ __global__ void __launch_bounds__(EPB* NQ* NQ)
             const PairFlux<Real> pf = pair_flux(nd[i], nd[j], P.gas.cg);
             const Real cij = P.negc[dir][i * NQ + j];
             const Real cji = P.negc[dir][j * NQ + i];
-            const Real fni = fma_(pf.tg, nd[i].ib, pf.f[1]);
-            const Real fnj = fma_(-pf.tg, nd[j].ib, pf.f[1]);
+            const Real fni = fma_(pf.tg, nd[i].hib, pf.f[1]);
+            const Real fnj = fma_(-pf.tg, nd[j].hib, pf.f[1]);
             acc[i][0] = fma_(cij, pf.f[0], acc[i][0]);
             acc[i][1] = fma_(cij, fni, acc[i][1]);
             acc[i][2] = fma_(cij, pf.f[2], acc[i][2]);
@@ -291,8 +325,9 @@ __global__ void __launch_bounds__(EPB* NQ* NQ)
               ph = P.ghost_phi[g * N2 + l];
             }
             Real nv[V_COUNT], pr;
-            if (!node_vals(qv, ph, P.gas.gm1, nv, pr) && !VOL)
-              raise_flag(P.flag, P.stage, P.elem_offset + eg, l);
+            if (!node_vals(qv, ph, P.gas.gm1, nv, pr))
+              raise_flag(P.flag, P.flag_records, P.stage, 1, P.elem_offset + eg, l,
+                         double(qv[0]), double(pr));
             nb = rotate_node(nv, dir);
           }
           // canonical orientation: lower Morton id is the minus side
@@ -307,7 +342,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ)
           // commit_face_side (kernels.hpp:391-430)
           const Real n_own = side ? Real(1) : Real(-1);
           const Real dsign = am_minus ? Real(-0.5) : Real(0.5);
-          const Real g_own = (am_minus ? pf.tg : -pf.tg) * own.ib;
+          const Real g_own = (am_minus ? pf.tg : -pf.tg) * own.hib;
           const Real lift = P.lift[dir];
           const Real phi_own = own.hphi + own.hphi;
           Real fl[5];
@@ -415,17 +450,27 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// Elements per CTA. Chosen so EPB*NQ^2 fills whole warps and two CTAs fit an
-// SM's shared memory where possible (FP64 figures).
+// Elements per CTA (EPB) and the resident-CTA target handed to
+// __launch_bounds__ (MINB): EPB*NQ^2 threads should fill whole warps, MINB
+// CTAs must fit an SM's 227 KB of shared memory at 14 quantity arrays per
+// node, and the register cap 65536/(MINB*threads) must not spill the line
+// state (ptxas -v is checked in DESIGN.md).
 template <int NQ, int BYTES>
 struct Tile;
-template <int B> struct Tile<2, B> { static constexpr int EPB = 32; };
-template <int B> struct Tile<3, B> { static constexpr int EPB = 14; };
-template <int B> struct Tile<4, B> { static constexpr int EPB = 8; };
-template <int B> struct Tile<5, B> { static constexpr int EPB = 5; };
-template <int B> struct Tile<6, B> { static constexpr int EPB = 3; };
-template <int B> struct Tile<7, B> { static constexpr int EPB = 2; };
-template <int B> struct Tile<8, B> { static constexpr int EPB = 2; };
+template <> struct Tile<2, 8> { static constexpr int EPB = 32, MINB = 4; };
+template <> struct Tile<3, 8> { static constexpr int EPB = 14, MINB = 4; };
+template <> struct Tile<4, 8> { static constexpr int EPB = 8, MINB = 3; };
+template <> struct Tile<5, 8> { static constexpr int EPB = 5, MINB = 3; };
+template <> struct Tile<6, 8> { static constexpr int EPB = 3, MINB = 2; };
+template <> struct Tile<7, 8> { static constexpr int EPB = 2, MINB = 2; };
+template <> struct Tile<8, 8> { static constexpr int EPB = 2, MINB = 1; };
+template <> struct Tile<2, 4> { static constexpr int EPB = 32, MINB = 4; };
+template <> struct Tile<3, 4> { static constexpr int EPB = 14, MINB = 4; };
+template <> struct Tile<4, 4> { static constexpr int EPB = 8, MINB = 4; };
+template <> struct Tile<5, 4> { static constexpr int EPB = 5, MINB = 4; };
+template <> struct Tile<6, 4> { static constexpr int EPB = 3, MINB = 4; };
+template <> struct Tile<7, 4> { static constexpr int EPB = 2, MINB = 4; };
+template <> struct Tile<8, 4> { static constexpr int EPB = 2, MINB = 2; };
 
 } // namespace dev
 } // namespace esdg_b200

@@ -1,13 +1,16 @@
 """GPU parity: the CUDA path, called through the C ABI, against the CPU
 oracle on identical inputs (-m gpu). Tolerances are stated per test.
 
-FP64 RHS tolerance: max_v max|d rhs_v| / S_v <= 2e-11 with S_v the abs-sum
-flux scale. Why not 1e-12: the reference forms logarithmic means and entropy
-jumps from DIFFERENCES of per-node logarithms (log_mean.hpp:62,
-physics.hpp:193-194); a 1-ulp difference between the device log and glibc's
-is amplified by 1/(2 xi) (xi = relative jump) in the means and by c T h ~ 4e7
-in the dissipation's energy slot. The reference itself moves by 1.2e-12 of
-max|rhs| when merely recompiled with FMA contraction.
+FP64 RHS tolerance: max_v max|d rhs_v| / S_v <= 2e-12, S_v = abs-sum flux
+scale (the magnitude of the terms the RHS adds up; oracle's flux_scale). The
+measured worst case over orders 1..7, bubble and random smooth states is
+5.9e-13 (tools/error_survey.py, profiles/r1_error_survey.txt). Normalising by
+max|rhs| instead is meaningless on near-hydrostatic states, where the tendency
+is a 1e-6 remainder of cancelling terms: there the same absolute differences
+read as up to 6e-10 (and the reference's own ladder gate trips on them,
+SURVEY.md section 4). Differences come from the device log being 1 ulp off
+glibc's in places, amplified by 1/(2 xi) in the logarithmic means.
+FP32: 3e-5 of S_v (measured worst 1.1e-5; FP32-vs-FP64 itself is ~1e-4).
 """
 import numpy as np
 import pytest
@@ -18,8 +21,8 @@ from helpers import both_configs, gas_pair, max_rel_diff, scaled_error, settings
 
 pytestmark = pytest.mark.gpu
 
-TOL64 = 2e-11   # of the abs-sum flux scale
-TOL32 = 5e-6    # FP32 GPU vs FP32 CPU
+TOL64 = 2e-12   # of the abs-sum flux scale
+TOL32 = 3e-5    # FP32 GPU vs FP32 CPU oracle, of the abs-sum flux scale
 
 
 def make(port, kind, margs, order, prec="f64", diss=True, cor=(0, 0.0, 0.0, 0.0), gravity=9.81,
@@ -66,8 +69,9 @@ def test_volume_rhs_fp64(port, order):
     want, got = o.volume_rhs(q), g.volume_rhs(q)
     # the reference's own bar between CPU variants is 1e-13 max_rel_diff
     # (test_kernels.cpp:69-93) and recompiling it with FMA contraction already
-    # moves it by 1.2e-12; device logs + FMAs: 5e-12
-    assert max_rel_diff(want, got) <= 5e-12
+    # moves it by 1.2e-12; device logs + FMAs measure
+    # 9e-14 / 3.3e-12 / 5.8e-12 at N = 2 / 4 / 5 on this state
+    assert max_rel_diff(want, got) <= 1e-11
     assert scaled_error(got, want, o.flux_scale(q)) <= TOL64
 
 
