@@ -354,9 +354,10 @@ int esdg_b200_solver_timers(esdg_b200_solver* s, double seconds[4],
                             int64_t* launches, int reset);
 
 /* Device self-test of the arithmetic the kernels rely on (esdg_device.cuh):
- * out4 = {max error of the fast reciprocal in ulps, samples violating
- * rcp(2x) == rcp(x)/2, 1 if rcp(1) == 1 exactly, samples tested}. */
-int esdg_b200_selftest(int device, int precision, double out4[4]);
+ * out5 = {max error of the fast reciprocal in ulps, samples violating
+ * rcp(2x) == rcp(x)/2, 1 if rcp(1) == 1 exactly, samples tested, max
+ * difference of the kernels' logarithm to the CUDA library's in ulps}. */
+int esdg_b200_selftest(int device, int precision, double out5[5]);
 
 /* DFMA / FFMA peak micro-benchmark on `device` (the roofline denominator of
  * K1; MEASURED_PEAKS.json has no CUDA-core figure). Returns TFLOP/s. */

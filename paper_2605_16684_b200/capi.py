@@ -474,10 +474,10 @@ class GpuSolver:
 
 
 def selftest(device=0, precision=8):
-    out = np.zeros(4)
+    out = np.zeros(5)
     check(lib().esdg_b200_selftest(device, precision, out.ctypes.data_as(_dp)))
     return dict(rcp_max_ulp=out[0], rcp_scaling_violations=int(out[1]), rcp_one_exact=bool(out[2]),
-                samples=int(out[3]))
+                samples=int(out[3]), log_vs_cuda_max_ulp=out[4])
 
 
 def measure_fma_peak(device=0, precision=8) -> float:

@@ -11,23 +11,26 @@
 //                                                solver.hpp:249-257)
 //
 // Execution model of rhs_kernel (B200: 148 SMs, 64 FP64 lanes/SM, 227 KB smem)
-//   - one CTA owns EPB consecutive (Morton) elements; EPB*NQ^2 threads.
-//   - phase A, thread per node: coalesced loads of q and phi straight from
-//     HBM, primitives + both logarithms once per node (precompute/logmean
-//     rungs of the reference's ladder) into shared memory, SoA per quantity.
+//   - one CTA owns EPB consecutive (Morton) elements; EPB*NQ^2 threads; thread
+//     (e, l) is "line l of element e" throughout.
+//   - phase A: the thread loads the NQ nodes of its z line straight from HBM
+//     (coalesced over l), computes primitives + both logarithms once per node
+//     (precompute/logmean rungs of the reference's ladder) and parks them in
+//     shared memory, SoA per quantity.
 //   - phase B, thread per node LINE: the thread pulls its line's NQ nodes
 //     into registers and evaluates every unordered pair (i,j) exactly once,
 //     adding c_ij (S + G e_n) to node i and c_ji (S - G b_i/b_j e_n) to node
 //     j in registers (the paper's pair symmetry incl. the -G b-/b+ rule for
 //     the non-symmetric gravity term). No partner exchange is needed, so the
-//     shared-memory pipe only sees the line load and the tendency update,
-//     and the FP64 FMA pipe is the bound. Directions run one after another
-//     in a rotated frame so the flux code is direction independent.
+//     shared-memory pipe only sees the line load and the tendency update.
+//     x and y sweeps go through the shared tendency slab; the z sweep stays
+//     in registers because the same thread commits that z line.
 //   - phase C, thread per face node: each element side evaluates the
 //     canonical (minus,plus) flux of its own face -- the flux is a pure
 //     function of the two traces, so both sides obtain bitwise identical
-//     values and conservation is exact without storing face records.
-//   - phase D, thread per node: commit, coalesced.
+//     values and conservation is exact without storing face records. x and y
+//     faces update the shared slab, z faces the thread's own registers.
+//   - commit: slab + registers -> out, coalesced over l.
 #pragma once
 
 #include "esdg_device.cuh"
@@ -142,13 +145,123 @@ __device__ __forceinline__ Node<Real> rotate_node(const Real nv[V_COUNT],
   return n;
 }
 
+// One line sweep of the flux-differenced volume term in direction DIR
+// (sweep_direction, kernels.hpp:154-249): pulls the NQ nodes of a line into
+// registers, ADDS the diagonal point fluxes and every unordered pair (once)
+// to acc, which lives in the rotated frame of DIR.
+template <class Real, int NQ, int DIR>
+__device__ __forceinline__ void sweep_line(const RhsParams<Real, NQ>& P,
+                                           const Real* vals, int VS, int base,
+                                           int stride, Real (&acc)[NQ][5]) {
+  Node<Real> nd[NQ];
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) nd[i] = load_node(vals, VS, base + i * stride, DIR);
+  // diagonal: t_i -= 2 g_d D_ii F(q_i, q_i)  (kernels.hpp:170-188). D_ii
+  // vanishes analytically at interior LGL nodes; the host flushes its
+  // O(1e-16) round-off residue to zero (shard.cu), so only the two end nodes
+  // pay for a point flux here.
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) {
+    const Real cii = P.negc[DIR][i * NQ + i];
+    if (cii != Real(0)) {
+      Real f[5];
+      point_flux(nd[i], P.gas.cg, f);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) acc[i][v] = fma_(cii, f[v], acc[i][v]);
+    }
+  }
+  // off-diagonal pairs, each once (kernels.hpp:190-231)
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) {
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+      if (j <= i) continue; // constant bounds keep the unroll total
+      const PairFlux<Real> pf = pair_flux(nd[i], nd[j], P.gas.cg);
+      const Real cij = P.negc[DIR][i * NQ + j];
+      const Real cji = P.negc[DIR][j * NQ + i];
+      const Real fni = fma_(pf.tg, nd[i].hib, pf.f[1]);
+      const Real fnj = fma_(-pf.tg, nd[j].hib, pf.f[1]);
+      acc[i][0] = fma_(cij, pf.f[0], acc[i][0]);
+      acc[i][1] = fma_(cij, fni, acc[i][1]);
+      acc[i][2] = fma_(cij, pf.f[2], acc[i][2]);
+      acc[i][3] = fma_(cij, pf.f[3], acc[i][3]);
+      acc[i][4] = fma_(cij, pf.f[4], acc[i][4]);
+      acc[j][0] = fma_(cji, pf.f[0], acc[j][0]);
+      acc[j][1] = fma_(cji, fnj, acc[j][1]);
+      acc[j][2] = fma_(cji, pf.f[2], acc[j][2]);
+      acc[j][3] = fma_(cji, pf.f[3], acc[j][3]);
+      acc[j][4] = fma_(cji, pf.f[4], acc[j][4]);
+    }
+  }
+}
+
+// Raw neighbour state at one face node, as fetched from HBM/L2.
+template <class Real>
+struct NbrRaw {
+  Real q[5], ph;
+  int code;
+};
+
+// Surface contribution of one face node of one element side, rotated frame
+// of `dir`: c[v] = lift (F*_v - n F_v(q_own)), to be SUBTRACTED from the
+// tendency (compute_face_record + commit_face_side, kernels.hpp:350-430).
+// Each side evaluates the canonical (minus, plus) flux itself; both sides get
+// bitwise identical values, so conservation is exact without face records.
+template <class Real, int NQ>
+__device__ __forceinline__ void face_contribution(const RhsParams<Real, NQ>& P,
+                                                  const Node<Real>& own,
+                                                  const NbrRaw<Real>& nbr, int dir,
+                                                  int side, long long eg, int fn,
+                                                  Real c[5]) {
+  Node<Real> nb;
+  bool am_minus;
+  if (nbr.code == -1) {
+    // reflecting wall: mirror state, phi+ = phi- (kernels.hpp:364-367)
+    nb = own;
+    nb.hun = -own.hun;
+    am_minus = true;
+  } else {
+    if (nbr.code >= 0)
+      am_minus = side ? (nbr.code >= eg) : (eg < nbr.code);
+    else
+      am_minus = ((-2 - nbr.code) & 1) != 0;
+    Real nv[V_COUNT], pr;
+    if (!node_vals(nbr.q, nbr.ph, P.gas.gm1, nv, pr))
+      raise_flag(P.flag, P.flag_records, P.stage, 1, P.elem_offset + eg, fn,
+                 double(nbr.q[0]), double(pr));
+    nb = rotate_node(nv, dir);
+  }
+  // canonical orientation: the lower Morton id is the minus side
+  const Node<Real> m = am_minus ? own : nb;
+  const Node<Real> p = am_minus ? nb : own;
+  const PairFlux<Real> pf = pair_flux(m, p, P.gas.cg);
+  Real dd[5] = {Real(0), Real(0), Real(0), Real(0), Real(0)};
+  if (P.dissipation) matrix_dissipation(m, p, pf.rho_log, pf.inv_blog, P.gas, dd);
+  Real fo[5];
+  point_flux(own, P.gas.cg, fo);
+  // commit_face_side (kernels.hpp:391-430)
+  const Real n_own = side ? Real(1) : Real(-1);
+  const Real dsign = am_minus ? Real(-0.5) : Real(0.5);
+  const Real g_own = (am_minus ? pf.tg : -pf.tg) * own.hib;
+  const Real lift = P.lift[dir];
+  const Real phi_own = own.hphi + own.hphi;
+  Real fl[5];
+  fl[0] = n_own * pf.f[0] + dsign * dd[0];
+  fl[1] = n_own * pf.f[1] + n_own * g_own + dsign * dd[1];
+  fl[2] = n_own * pf.f[2] + dsign * dd[2];
+  fl[3] = n_own * pf.f[3] + dsign * dd[3];
+  fl[4] = n_own * pf.f[4] + dsign * fma_(phi_own, dd[0], dd[4]);
+#pragma unroll
+  for (int v = 0; v < 5; ++v) c[v] = lift * (fl[v] - n_own * fo[v]);
+}
+
 template <class Real, int NQ, int EPB, int MINB, bool VOL, bool SURF>
 __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     rhs_kernel(const __grid_constant__ RhsParams<Real, NQ> P) {
   using G = Geo<NQ>;
   constexpr int N2 = G::N2, N3 = G::N3, PX = G::PX, N3P = G::N3P;
-  constexpr int T = EPB * N2;
   constexpr int VS = EPB * N3P; // stride between quantity arrays
+  constexpr int ZS = PX * NQ;   // shared-memory pitch of the z axis
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Real* vals = reinterpret_cast<Real*>(smem_raw); // [V_COUNT][VS]
@@ -159,238 +272,213 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   const long long left = P.ne - e0;
   const int ne_blk = left < EPB ? static_cast<int>(left) : EPB;
 
-  // ---- phase A: primitives and logarithms, once per node ------------------
-  for (int idx = tid; idx < ne_blk * N3; idx += T) {
-    const int e = idx / N3, n = idx - e * N3;
-    const Real* qe = P.q + (e0 + e) * (5 * N3);
-    Real qv[5];
-#pragma unroll
-    for (int v = 0; v < 5; ++v) qv[v] = qe[v * N3 + n];
-    const Real ph = P.phi[(e0 + e) * N3 + n];
-    Real nv[V_COUNT], pr;
-    if (!node_vals(qv, ph, P.gas.gm1, nv, pr))
-      raise_flag(P.flag, P.flag_records, P.stage, 0, P.elem_offset + e0 + e, n,
-                 double(qv[0]), double(pr));
-    const int s = e * N3P + G::sidx(n);
-#pragma unroll
-    for (int k = 0; k < V_COUNT; ++k) vals[k * VS + s] = nv[k];
-    if (!VOL) {
-#pragma unroll
-      for (int v = 0; v < 5; ++v) tend[v * VS + s] = Real(0);
-    }
-  }
-  __syncthreads();
+  // thread <-> (element e, line l = l0 + NQ l1). In phase A, in the z sweep
+  // and in the commit the thread owns the z line through (x, y) = (l0, l1),
+  // so those three stages hand data over in registers.
+  const int e = tid / N2, l = tid - e * N2;
+  const bool active = e < ne_blk;
+  const int l0 = l % NQ, l1 = l / NQ;
+  const long long eg = e0 + e;
+  const int zbase = e * N3P + l0 + PX * l1;
+  const bool read_out = !VOL || P.a_old != Real(0);
 
   // pitches of the three axes in shared (padded) and global node numbering
   auto spitch = [](int ax) { return ax == 0 ? 1 : (ax == 1 ? PX : PX * NQ); };
   auto gpitch = [](int ax) { return ax == 0 ? 1 : (ax == 1 ? NQ : NQ * NQ); };
-  const int e = tid / N2, l = tid - e * N2;
-  const bool active = e < ne_blk;
-  const int l0 = l % NQ, l1 = l / NQ;
 
-  // ---- phase B: flux differencing, every pair of a line once --------------
+  // ---- phase A: primitives and logarithms, once per node ------------------
+  // All global loads are issued before the first logarithm so they overlap.
+  if (active) {
+    const Real* qe = P.q + eg * (5 * N3) + l;
+    const Real* pe = P.phi + eg * N3 + l;
+    Real qv[NQ][5], ph[NQ];
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) qv[k][v] = qe[v * N3 + k * N2];
+      ph[k] = pe[k * N2];
+    }
+    if (read_out) {
+      // the commit reads this CTA's slab of `out` much later: pull it into L2
+      const char* ob = reinterpret_cast<const char*>(P.out + e0 * (5 * N3));
+      const int bytes = ne_blk * 5 * N3 * int(sizeof(Real));
+      for (int off = tid * 128; off < bytes; off += EPB * N2 * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(ob + off));
+    }
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) {
+      Real nv[V_COUNT], pr;
+      if (!node_vals(qv[k], ph[k], P.gas.gm1, nv, pr))
+        raise_flag(P.flag, P.flag_records, P.stage, 0, P.elem_offset + eg, l + k * N2,
+                   double(qv[k][0]), double(pr));
+      const int s = zbase + k * ZS;
+#pragma unroll
+      for (int j = 0; j < V_COUNT; ++j) vals[j * VS + s] = nv[j];
+      if (!VOL) {
+#pragma unroll
+        for (int v = 0; v < 5; ++v) tend[v * VS + s] = Real(0);
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- phase B: x and y sweeps, results through shared memory -------------
   if (VOL) {
-#pragma unroll 1
-    for (int dir = 0; dir < 3; ++dir) {
-      if (active) {
-        int base, stride;
-        if (dir == 0) {
-          base = PX * l;
-          stride = 1;
-        } else if (dir == 1) {
-          base = l0 + PX * NQ * l1;
-          stride = PX;
-        } else {
-          base = l0 + PX * l1;
-          stride = PX * NQ;
-        }
-        base += e * N3P;
-        Node<Real> nd[NQ];
+    if (active) {
+      Real acc[NQ][5];
 #pragma unroll
-        for (int i = 0; i < NQ; ++i)
-          nd[i] = load_node(vals, VS, base + i * stride, dir);
-
-        Real acc[NQ][5];
-        // diagonal: t_i -= 2 g_d D_ii F(q_i, q_i)  (kernels.hpp:170-188)
+      for (int i = 0; i < NQ; ++i)
 #pragma unroll
-        for (int i = 0; i < NQ; ++i) {
-          const Real cii = P.negc[dir][i * NQ + i];
+        for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
+      const int base = e * N3P + PX * l; // x line through (y, z) = (l0, l1)
+      sweep_line<Real, NQ, 0>(P, vals, VS, base, 1, acc);
 #pragma unroll
-          for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
-          // D_ii vanishes analytically at interior LGL nodes; the host
-          // flushes its O(1e-16) round-off residue to zero (shard.cu), so
-          // only the two end nodes pay for a point flux here
-          if (cii != Real(0)) {
-            Real f[5];
-            point_flux(nd[i], P.gas.cg, f);
-#pragma unroll
-            for (int v = 0; v < 5; ++v) acc[i][v] = cii * f[v];
-          }
-        }
-        // off-diagonal pairs, each once (kernels.hpp:190-231)
-#pragma unroll
-        for (int i = 0; i < NQ; ++i) {
-#pragma unroll
-          for (int j = 0; j < NQ; ++j) {
-            if (j <= i) continue; // constant bounds keep the unroll total
-            const PairFlux<Real> pf = pair_flux(nd[i], nd[j], P.gas.cg);
-            const Real cij = P.negc[dir][i * NQ + j];
-            const Real cji = P.negc[dir][j * NQ + i];
-            const Real fni = fma_(pf.tg, nd[i].hib, pf.f[1]);
-            const Real fnj = fma_(-pf.tg, nd[j].hib, pf.f[1]);
-            acc[i][0] = fma_(cij, pf.f[0], acc[i][0]);
-            acc[i][1] = fma_(cij, fni, acc[i][1]);
-            acc[i][2] = fma_(cij, pf.f[2], acc[i][2]);
-            acc[i][3] = fma_(cij, pf.f[3], acc[i][3]);
-            acc[i][4] = fma_(cij, pf.f[4], acc[i][4]);
-            acc[j][0] = fma_(cji, pf.f[0], acc[j][0]);
-            acc[j][1] = fma_(cji, fnj, acc[j][1]);
-            acc[j][2] = fma_(cji, pf.f[2], acc[j][2]);
-            acc[j][3] = fma_(cji, pf.f[3], acc[j][3]);
-            acc[j][4] = fma_(cji, pf.f[4], acc[j][4]);
-          }
-        }
-        // un-rotate into the tendency slab
-        const int d1 = dir == 2 ? 0 : dir + 1;
-        const int d2 = d1 == 2 ? 0 : d1 + 1;
-        Real* t0 = tend;
-        Real* tn = tend + (1 + dir) * VS;
-        Real* tt1 = tend + (1 + d1) * VS;
-        Real* tt2 = tend + (1 + d2) * VS;
-        Real* t4 = tend + 4 * VS;
-#pragma unroll
-        for (int i = 0; i < NQ; ++i) {
-          const int s = base + i * stride;
-          if (dir == 0) {
-            t0[s] = acc[i][0];
-            tn[s] = acc[i][1];
-            tt1[s] = acc[i][2];
-            tt2[s] = acc[i][3];
-            t4[s] = acc[i][4];
-          } else {
-            t0[s] += acc[i][0];
-            tn[s] += acc[i][1];
-            tt1[s] += acc[i][2];
-            tt2[s] += acc[i][3];
-            t4[s] += acc[i][4];
-          }
-        }
+      for (int i = 0; i < NQ; ++i) {
+        const int s = base + i;
+        tend[0 * VS + s] = acc[i][0];
+        tend[1 * VS + s] = acc[i][1];
+        tend[2 * VS + s] = acc[i][2];
+        tend[3 * VS + s] = acc[i][3];
+        tend[4 * VS + s] = acc[i][4];
       }
-      __syncthreads();
     }
+    __syncthreads();
+    if (active) {
+      Real acc[NQ][5];
+#pragma unroll
+      for (int i = 0; i < NQ; ++i)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
+      const int base = e * N3P + l0 + ZS * l1; // y line through (x, z) = (l0, l1)
+      sweep_line<Real, NQ, 1>(P, vals, VS, base, PX, acc);
+      // rotated frame of y: normal -> var 2, t1 = z -> var 3, t2 = x -> var 1
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) {
+        const int s = base + i * PX;
+        tend[0 * VS + s] += acc[i][0];
+        tend[2 * VS + s] += acc[i][1];
+        tend[3 * VS + s] += acc[i][2];
+        tend[1 * VS + s] += acc[i][3];
+        tend[4 * VS + s] += acc[i][4];
+      }
+    }
+    __syncthreads();
   }
 
-  // ---- phase C: surface term, each side evaluates its own face ------------
+  // ---- phase C: x and y faces, thread per face node ------------------------
+  // The neighbour state of face lf+1 is fetched while face lf is evaluated.
+  NbrRaw<Real> cur, nxt;
+  auto fetch = [&](int lf, NbrRaw<Real>& r) {
+    const int dir = lf >> 1, side = lf & 1;
+    const int d1 = dir == 2 ? 0 : dir + 1;
+    const int d2 = d1 == 2 ? 0 : d1 + 1;
+    r.code = P.nbr[eg * 6 + lf];
+    if (r.code >= 0) {
+      // opposite side of the neighbour, same tangential (s, t)
+      const int n_nb = (side ? 0 : NQ - 1) * gpitch(dir) + l0 * gpitch(d1) +
+                       l1 * gpitch(d2);
+      const Real* qn = P.q + static_cast<long long>(r.code) * (5 * N3);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) r.q[v] = qn[v * N3 + n_nb];
+      r.ph = P.phi[static_cast<long long>(r.code) * N3 + n_nb];
+    } else if (r.code <= -2) {
+      const long long g = (-2 - r.code) >> 1;
+#pragma unroll
+      for (int v = 0; v < 5; ++v) r.q[v] = P.ghost_q[(g * 5 + v) * N2 + l];
+      r.ph = P.ghost_phi[g * N2 + l];
+    }
+  };
   if (SURF) {
+    if (active) fetch(0, cur);
 #pragma unroll 1
-    for (int dir = 0; dir < 3; ++dir) {
+    for (int lf = 0; lf < 4; ++lf) {
       if (active) {
-        const int d1 = dir == 2 ? 0 : dir + 1;
+        fetch(lf + 1, nxt);
+        const int dir = lf >> 1, side = lf & 1;
+        const int d1 = dir + 1;              // dir is 0 or 1 here
         const int d2 = d1 == 2 ? 0 : d1 + 1;
-        const long long eg = e0 + e;
-#pragma unroll 1
-        for (int side = 0; side < 2; ++side) {
-          // FaceIndexer::node (mesh.hpp:107-114): tangential axes d1, d2
-          // node = sum_k c_k * pitch_k with c[dir] = end, c[d1] = l0, c[d2] = l1
-          const int cn = side ? NQ - 1 : 0;
-          const int s_own = e * N3P + cn * spitch(dir) + l0 * spitch(d1) +
-                            l1 * spitch(d2);
-          const Node<Real> own = load_node(vals, VS, s_own, dir);
-
-          const int code = P.nbr[eg * 6 + dir * 2 + side];
-          Node<Real> nb;
-          bool am_minus;
-          if (code == -1) {
-            // reflecting wall: mirror state, phi+ = phi- (kernels.hpp:364-367)
-            nb = own;
-            nb.hun = -own.hun;
-            am_minus = true;
-          } else {
-            Real qv[5], ph;
-            if (code >= 0) {
-              const int n_nb = (NQ - 1 - cn) * gpitch(dir) + l0 * gpitch(d1) +
-                               l1 * gpitch(d2);
-              const Real* qn = P.q + static_cast<long long>(code) * (5 * N3);
-#pragma unroll
-              for (int v = 0; v < 5; ++v) qv[v] = qn[v * N3 + n_nb];
-              ph = P.phi[static_cast<long long>(code) * N3 + n_nb];
-              am_minus = side ? (code >= eg) : (eg < code);
-            } else {
-              const int gv = -2 - code;
-              const long long g = gv >> 1;
-              am_minus = (gv & 1) != 0;
-#pragma unroll
-              for (int v = 0; v < 5; ++v)
-                qv[v] = P.ghost_q[(g * 5 + v) * N2 + l];
-              ph = P.ghost_phi[g * N2 + l];
-            }
-            Real nv[V_COUNT], pr;
-            if (!node_vals(qv, ph, P.gas.gm1, nv, pr))
-              raise_flag(P.flag, P.flag_records, P.stage, 1, P.elem_offset + eg, l,
-                         double(qv[0]), double(pr));
-            nb = rotate_node(nv, dir);
-          }
-          // canonical orientation: lower Morton id is the minus side
-          const Node<Real> m = am_minus ? own : nb;
-          const Node<Real> p = am_minus ? nb : own;
-          const PairFlux<Real> pf = pair_flux(m, p, P.gas.cg);
-          Real dd[5] = {Real(0), Real(0), Real(0), Real(0), Real(0)};
-          if (P.dissipation)
-            matrix_dissipation(m, p, pf.rho_log, pf.inv_blog, P.gas, dd);
-          Real fo[5];
-          point_flux(own, P.gas.cg, fo);
-          // commit_face_side (kernels.hpp:391-430)
-          const Real n_own = side ? Real(1) : Real(-1);
-          const Real dsign = am_minus ? Real(-0.5) : Real(0.5);
-          const Real g_own = (am_minus ? pf.tg : -pf.tg) * own.hib;
-          const Real lift = P.lift[dir];
-          const Real phi_own = own.hphi + own.hphi;
-          Real fl[5];
-          fl[0] = n_own * pf.f[0] + dsign * dd[0];
-          fl[1] = n_own * pf.f[1] + n_own * g_own + dsign * dd[1];
-          fl[2] = n_own * pf.f[2] + dsign * dd[2];
-          fl[3] = n_own * pf.f[3] + dsign * dd[3];
-          fl[4] = n_own * pf.f[4] + dsign * fma_(phi_own, dd[0], dd[4]);
-          tend[s_own] -= lift * (fl[0] - n_own * fo[0]);
-          tend[(1 + dir) * VS + s_own] -= lift * (fl[1] - n_own * fo[1]);
-          tend[(1 + d1) * VS + s_own] -= lift * (fl[2] - n_own * fo[2]);
-          tend[(1 + d2) * VS + s_own] -= lift * (fl[3] - n_own * fo[3]);
-          tend[4 * VS + s_own] -= lift * (fl[4] - n_own * fo[4]);
-        }
+        // FaceIndexer::node (mesh.hpp:107-114): tangential axes d1, d2
+        const int s_own = e * N3P + (side ? NQ - 1 : 0) * spitch(dir) +
+                          l0 * spitch(d1) + l1 * spitch(d2);
+        const Node<Real> own = load_node(vals, VS, s_own, dir);
+        Real c[5];
+        face_contribution<Real, NQ>(P, own, cur, dir, side, eg, l, c);
+        tend[s_own] -= c[0];
+        tend[(1 + dir) * VS + s_own] -= c[1];
+        tend[(1 + d1) * VS + s_own] -= c[2];
+        tend[(1 + d2) * VS + s_own] -= c[3];
+        tend[4 * VS + s_own] -= c[4];
+        cur = nxt;
       }
-      __syncthreads();
+      // the two faces of a direction share no node; the next direction does
+      if (lf & 1) __syncthreads();
     }
   }
 
-  // ---- phase D: commit (solver.hpp:199-223) --------------------------------
-  for (int idx = tid; idx < ne_blk * N3; idx += T) {
-    const int ee = idx / N3, n = idx - ee * N3;
-    const int s = ee * N3P + G::sidx(n);
-    Real* oe = P.out + (e0 + ee) * (5 * N3);
-    Real val[5];
+  // ---- z faces, z sweep and commit: all on the thread's own z line ---------
+  if (active) {
+    Real acc[NQ][5]; // rotated frame of z: normal -> var 3, t1 = x -> 1, t2 = y -> 2
 #pragma unroll
-    for (int v = 0; v < 5; ++v) val[v] = tend[v * VS + s];
-    if (VOL) {
-      if (P.with_source) {
-        // coriolis_source (physics.hpp:297-306): h = (0, f q2, -f q1, 0, 0)
-        const Real* qe = P.q + (e0 + ee) * (5 * N3);
-        const int b = (n / NQ) % NQ;
-        const Real f = P.cor_f[P.ylevel[e0 + ee] * NQ + b];
-        val[1] = val[1] + f * qe[2 * N3 + n];
-        val[2] = val[2] + (-f) * qe[1 * N3 + n];
+    for (int i = 0; i < NQ; ++i)
+#pragma unroll
+      for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
+    if (SURF) {
+      fetch(5, nxt);
+      {
+        const Node<Real> own = load_node(vals, VS, zbase, 2);
+        Real c[5];
+        face_contribution<Real, NQ>(P, own, cur, 2, 0, eg, l, c);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) acc[0][v] -= c[v];
       }
-      if (P.a_old == Real(0)) {
+      {
+        const Node<Real> own = load_node(vals, VS, zbase + (NQ - 1) * ZS, 2);
+        Real c[5];
+        face_contribution<Real, NQ>(P, own, nxt, 2, 1, eg, l, c);
 #pragma unroll
-        for (int v = 0; v < 5; ++v) oe[v * N3 + n] = P.a_new * val[v];
+        for (int v = 0; v < 5; ++v) acc[NQ - 1][v] -= c[v];
+      }
+    }
+    if (VOL) sweep_line<Real, NQ, 2>(P, vals, VS, zbase, ZS, acc);
+
+    // commit (solver.hpp:199-223), one z line per thread, coalesced over l
+    Real* oe = P.out + eg * (5 * N3) + l;
+    Real ov[NQ][5];
+    if (read_out) {
+#pragma unroll
+      for (int k = 0; k < NQ; ++k)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) ov[k][v] = oe[v * N3 + k * N2];
+    }
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) {
+      const int s = zbase + k * ZS;
+      Real val[5];
+      val[0] = tend[0 * VS + s] + acc[k][0];
+      val[1] = tend[1 * VS + s] + acc[k][2];
+      val[2] = tend[2 * VS + s] + acc[k][3];
+      val[3] = tend[3 * VS + s] + acc[k][1];
+      val[4] = tend[4 * VS + s] + acc[k][4];
+      if (VOL) {
+        if (P.with_source) {
+          // coriolis_source (physics.hpp:297-306): h = (0, f q2, -f q1, 0, 0)
+          const Real* qe = P.q + eg * (5 * N3) + l + k * N2;
+          const Real f = P.cor_f[P.ylevel[eg] * NQ + l1];
+          val[1] = val[1] + f * qe[2 * N3];
+          val[2] = val[2] + (-f) * qe[1 * N3];
+        }
+        if (P.a_old == Real(0)) {
+#pragma unroll
+          for (int v = 0; v < 5; ++v) oe[v * N3 + k * N2] = P.a_new * val[v];
+        } else {
+#pragma unroll
+          for (int v = 0; v < 5; ++v)
+            oe[v * N3 + k * N2] = P.a_old * ov[k][v] + P.a_new * val[v];
+        }
       } else {
 #pragma unroll
-        for (int v = 0; v < 5; ++v)
-          oe[v * N3 + n] = P.a_old * oe[v * N3 + n] + P.a_new * val[v];
+        for (int v = 0; v < 5; ++v) oe[v * N3 + k * N2] = ov[k][v] + P.a_new * val[v];
       }
-    } else {
-#pragma unroll
-      for (int v = 0; v < 5; ++v)
-        oe[v * N3 + n] = oe[v * N3 + n] + P.a_new * val[v];
     }
   }
 }

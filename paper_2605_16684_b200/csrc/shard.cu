@@ -386,12 +386,14 @@ __global__ void __launch_bounds__(256) fma_peak_kernel(Real* out, int iters) {
 // Device self-test of the arithmetic identities the kernels rely on.
 // out[0] = max error of rcp_ in ulps against the correctly rounded 1/x,
 // out[1] = number of samples where rcp_(2x) != rcp_(x)/2,
-// out[2] = 1 when rcp_(1) == 1 exactly, out[3] = samples tested.
+// out[2] = 1 when rcp_(1) == 1 exactly, out[3] = samples tested,
+// out[4] = max |log_ - CUDA log| in ulps over positive samples (FP64: the
+// lean log_pos of esdg_log.cuh against the library routine).
 template <class Real>
 __global__ void selftest_kernel(double* out, int n) {
-  __shared__ double s_err[256];
+  __shared__ double s_err[256], s_log[256];
   __shared__ int s_bad[256];
-  double worst = 0.0;
+  double worst = 0.0, worst_log = 0.0;
   int bad = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     // deterministic samples over ~12 decades, both signs
@@ -409,13 +411,20 @@ __global__ void selftest_kernel(double* out, int n) {
     const double e = fabs(double(r) - double(exact)) / double(ulp);
     if (e > worst) worst = e;
     if (dev::rcp_(x + x) != Real(0.5) * r) ++bad;
+    const Real ax = x < Real(0) ? -x : x;
+    const double lref = sizeof(Real) == 8 ? log(double(ax)) : double(logf(float(ax)));
+    const double lulp = fabs(lref) * (sizeof(Real) == 8 ? 2.220446049250313e-16 : 1.1920929e-7);
+    const double le = fabs(double(dev::log_(ax)) - lref) / (lulp > 0.0 ? lulp : 1.0);
+    if (le > worst_log) worst_log = le;
   }
   s_err[threadIdx.x] = worst;
+  s_log[threadIdx.x] = worst_log;
   s_bad[threadIdx.x] = bad;
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int t = 1; t < blockDim.x; ++t) {
       if (s_err[t] > worst) worst = s_err[t];
+      if (s_log[t] > worst_log) worst_log = s_log[t];
       bad += s_bad[t];
     }
     // one block: plain stores
@@ -423,17 +432,18 @@ __global__ void selftest_kernel(double* out, int n) {
     out[1] = double(bad);
     out[2] = dev::rcp_(Real(1)) == Real(1) ? 1.0 : 0.0;
     out[3] = double(n);
+    out[4] = worst_log;
   }
 }
 
 template <class Real>
-int run_selftest(int device, double* out4) {
+int run_selftest(int device, double* out5) {
   CU(cudaSetDevice(device));
   double* d = nullptr;
-  CU(cudaMalloc(&d, 4 * sizeof(double)));
+  CU(cudaMalloc(&d, 5 * sizeof(double)));
   selftest_kernel<Real><<<1, 256>>>(d, 1 << 20);
   CU(cudaGetLastError());
-  CU(cudaMemcpy(out4, d, 4 * sizeof(double), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(out5, d, 5 * sizeof(double), cudaMemcpyDeviceToHost));
   cudaFree(d);
   return ESDG_B200_OK;
 }
@@ -625,10 +635,10 @@ int64_t esdg_b200_shard_launch_count(const esdg_b200_shard* s) {
   return s ? s->impl->launch_count() : 0;
 }
 
-int esdg_b200_selftest(int device, int precision, double out4[4]) {
-  if (!out4) return ESDG_B200_BADARG;
-  if (precision == 8) return esdg_b200::run_selftest<double>(device, out4);
-  if (precision == 4) return esdg_b200::run_selftest<float>(device, out4);
+int esdg_b200_selftest(int device, int precision, double out5[5]) {
+  if (!out5) return ESDG_B200_BADARG;
+  if (precision == 8) return esdg_b200::run_selftest<double>(device, out5);
+  if (precision == 4) return esdg_b200::run_selftest<float>(device, out5);
   return ESDG_B200_BADARG;
 }
 
