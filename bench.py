@@ -42,7 +42,7 @@ def parse_args():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--order", type=int, default=4)
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
-    ap.add_argument("--path", default="fused", choices=["fused", "split"])
+    ap.add_argument("--path", default="stage", choices=["stage", "fused", "split"])
     ap.add_argument("--refinement", type=int, default=5)
     ap.add_argument("--base", type=int, nargs=3, default=None,
                     help="override the base lattice (default: configs[4] table)")
@@ -247,7 +247,7 @@ def main_b200(args, rank, local_rank, world):
     else:
         solver = capi.GpuSolver(mesh, args.order, args.precision, settings=settings, devices=[device])
         exchange = None
-    solver.set_path(capi.PATH_FUSED if args.path == "fused" else capi.PATH_SPLIT)
+    solver.set_path({"stage": capi.PATH_STAGE, "fused": capi.PATH_FUSED, "split": capi.PATH_SPLIT}[args.path])
     solver.init_case(case_id)
     dt_local = solver.compute_dt(0.5)
     if world > 1:

@@ -154,6 +154,14 @@ int esdg_b200_shard_rhs_fused(esdg_b200_shard* s, int src, int dst,
                               double a_old, double a_new, int stage,
                               void* stream);
 
+/* K1+K2+K3, one whole LSRK stage in one kernel (lsrk_step's loop body,
+ * time_integration.hpp:43-49): k <- a_old k + a_new RHS(q); q <- q + b k.
+ * q is double buffered inside the shard (neighbouring elements still read
+ * the old faces while an element commits), so REG_Q always names the current
+ * buffer and the shard holds three state registers once this is used. */
+int esdg_b200_shard_stage_fused(esdg_b200_shard* s, double a_old, double a_new,
+                                double b, int stage, void* stream);
+
 /* K3: q <- q + b k. Replaces Solver::axpy (solver.hpp:342-353). */
 int esdg_b200_shard_axpy(esdg_b200_shard* s, double b, void* stream);
 
@@ -255,7 +263,9 @@ enum {
 
 enum {
   ESDG_B200_PATH_SPLIT = 0, /* K1 then K2, as the reference structures it */
-  ESDG_B200_PATH_FUSED = 1  /* K1+K2 in one kernel */
+  ESDG_B200_PATH_FUSED = 1, /* K1+K2 in one kernel */
+  ESDG_B200_PATH_STAGE = 2  /* step(): K1+K2+K3 in one kernel per stage;
+                               rhs()/assemble_rhs() behave like PATH_FUSED */
 };
 
 typedef struct esdg_b200_solver esdg_b200_solver;

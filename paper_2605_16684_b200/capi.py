@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(CSRC, "libesdg_b200.so")
 
 OK, NONPHYSICAL, CUDA, BADARG = 0, 1, 2, 3
 REG_Q, REG_K = 0, 1
-PATH_SPLIT, PATH_FUSED = 0, 1
+PATH_SPLIT, PATH_FUSED, PATH_STAGE = 0, 1, 2
 (CASE_BUBBLE_SHARP, CASE_BUBBLE_SMOOTH, CASE_HYDROSTATIC, CASE_ENTROPY_TEST,
  CASE_CONSTANT, CASE_BAROCLINIC) = range(6)
 
@@ -93,6 +93,7 @@ SIGNATURES = {
     "esdg_b200_shard_volume": (_i, [_vp, _i, _i, _d, _d, _i, _i, _vp]),
     "esdg_b200_shard_surface": (_i, [_vp, _i, _i, _d, _i, _vp]),
     "esdg_b200_shard_rhs_fused": (_i, [_vp, _i, _i, _d, _d, _i, _vp]),
+    "esdg_b200_shard_stage_fused": (_i, [_vp, _d, _d, _d, _i, _vp]),
     "esdg_b200_shard_axpy": (_i, [_vp, _d, _vp]),
     "esdg_b200_shard_check": (_i, [_vp, _vp, C.POINTER(Error)]),
     "esdg_b200_shard_launch_count": (_i64, [_vp]),

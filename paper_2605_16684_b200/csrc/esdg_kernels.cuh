@@ -43,6 +43,7 @@ struct FlagRecord;
 template <class Real, int NQ>
 struct RhsParams {
   const Real* q;
+  Real* q_next; // fused stage update: q_next = q + b_upd * out_new (may be null)
   Real* out;
   const Real* phi;
   const int32_t* nbr;
@@ -54,7 +55,7 @@ struct RhsParams {
   FlagRecord* flag_records;
   long long ne;
   long long elem_offset;
-  Real a_old, a_new;
+  Real a_old, a_new, b_upd;
   GasParams<Real> gas;
   Real negc[3][NQ * NQ]; // -(2 g_d D_ij), kernels.hpp:187, 224-225
   Real lift[3];          // Operators::face_coef, kernels.hpp:86-88
@@ -205,8 +206,17 @@ struct NbrRaw {
 // Surface contribution of one face node of one element side, rotated frame
 // of `dir`: c[v] = lift (F*_v - n F_v(q_own)), to be SUBTRACTED from the
 // tendency (compute_face_record + commit_face_side, kernels.hpp:350-430).
-// Each side evaluates the canonical (minus, plus) flux itself; both sides get
-// bitwise identical values, so conservation is exact without face records.
+//
+// Each side evaluates its own face; no face records are stored. That is
+// exact because pair_flux and matrix_dissipation are written so that swapping
+// their arguments gives bitwise the same symmetric part and bitwise the
+// negated gravity / dissipation part (sums and products commute, differences
+// and rcp_ negate exactly, see esdg_device.cuh). With (own, nbr) as argument
+// order the reference's canonical record (minus = lower Morton id) reduces to
+//   am_minus:  n (S + G e_n)        - D(own,nbr)/2,  G = tg hib_own
+//   otherwise: n (S - G' b-/b+ e_n) + D(nbr,own)/2 = the same expression,
+// so the orientation never has to be looked at, and the two sides of a face
+// subtract exactly opposite numbers: conservation is exact.
 template <class Real, int NQ>
 __device__ __forceinline__ void face_contribution(const RhsParams<Real, NQ>& P,
                                                   const Node<Real>& own,
@@ -214,43 +224,33 @@ __device__ __forceinline__ void face_contribution(const RhsParams<Real, NQ>& P,
                                                   int side, long long eg, int fn,
                                                   Real c[5]) {
   Node<Real> nb;
-  bool am_minus;
   if (nbr.code == -1) {
     // reflecting wall: mirror state, phi+ = phi- (kernels.hpp:364-367)
     nb = own;
     nb.hun = -own.hun;
-    am_minus = true;
   } else {
-    if (nbr.code >= 0)
-      am_minus = side ? (nbr.code >= eg) : (eg < nbr.code);
-    else
-      am_minus = ((-2 - nbr.code) & 1) != 0;
     Real nv[V_COUNT], pr;
     if (!node_vals(nbr.q, nbr.ph, P.gas.gm1, nv, pr))
       raise_flag(P.flag, P.flag_records, P.stage, 1, P.elem_offset + eg, fn,
                  double(nbr.q[0]), double(pr));
     nb = rotate_node(nv, dir);
   }
-  // canonical orientation: the lower Morton id is the minus side
-  const Node<Real> m = am_minus ? own : nb;
-  const Node<Real> p = am_minus ? nb : own;
-  const PairFlux<Real> pf = pair_flux(m, p, P.gas.cg);
+  const PairFlux<Real> pf = pair_flux(own, nb, P.gas.cg);
   Real dd[5] = {Real(0), Real(0), Real(0), Real(0), Real(0)};
-  if (P.dissipation) matrix_dissipation(m, p, pf.rho_log, pf.inv_blog, P.gas, dd);
+  if (P.dissipation) matrix_dissipation(own, nb, pf.rho_log, pf.inv_blog, P.gas, dd);
   Real fo[5];
   point_flux(own, P.gas.cg, fo);
   // commit_face_side (kernels.hpp:391-430)
   const Real n_own = side ? Real(1) : Real(-1);
-  const Real dsign = am_minus ? Real(-0.5) : Real(0.5);
-  const Real g_own = (am_minus ? pf.tg : -pf.tg) * own.hib;
+  const Real g_own = pf.tg * own.hib;
   const Real lift = P.lift[dir];
   const Real phi_own = own.hphi + own.hphi;
   Real fl[5];
-  fl[0] = n_own * pf.f[0] + dsign * dd[0];
-  fl[1] = n_own * pf.f[1] + n_own * g_own + dsign * dd[1];
-  fl[2] = n_own * pf.f[2] + dsign * dd[2];
-  fl[3] = n_own * pf.f[3] + dsign * dd[3];
-  fl[4] = n_own * pf.f[4] + dsign * fma_(phi_own, dd[0], dd[4]);
+  fl[0] = n_own * pf.f[0] - Real(0.5) * dd[0];
+  fl[1] = n_own * pf.f[1] + n_own * g_own - Real(0.5) * dd[1];
+  fl[2] = n_own * pf.f[2] - Real(0.5) * dd[2];
+  fl[3] = n_own * pf.f[3] - Real(0.5) * dd[3];
+  fl[4] = n_own * pf.f[4] - Real(0.5) * fma_(phi_own, dd[0], dd[4]);
 #pragma unroll
   for (int v = 0; v < 5; ++v) c[v] = lift * (fl[v] - n_own * fo[v]);
 }
@@ -322,51 +322,8 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   }
   __syncthreads();
 
-  // ---- phase B: x and y sweeps, results through shared memory -------------
-  if (VOL) {
-    if (active) {
-      Real acc[NQ][5];
-#pragma unroll
-      for (int i = 0; i < NQ; ++i)
-#pragma unroll
-        for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
-      const int base = e * N3P + PX * l; // x line through (y, z) = (l0, l1)
-      sweep_line<Real, NQ, 0>(P, vals, VS, base, 1, acc);
-#pragma unroll
-      for (int i = 0; i < NQ; ++i) {
-        const int s = base + i;
-        tend[0 * VS + s] = acc[i][0];
-        tend[1 * VS + s] = acc[i][1];
-        tend[2 * VS + s] = acc[i][2];
-        tend[3 * VS + s] = acc[i][3];
-        tend[4 * VS + s] = acc[i][4];
-      }
-    }
-    __syncthreads();
-    if (active) {
-      Real acc[NQ][5];
-#pragma unroll
-      for (int i = 0; i < NQ; ++i)
-#pragma unroll
-        for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
-      const int base = e * N3P + l0 + ZS * l1; // y line through (x, z) = (l0, l1)
-      sweep_line<Real, NQ, 1>(P, vals, VS, base, PX, acc);
-      // rotated frame of y: normal -> var 2, t1 = z -> var 3, t2 = x -> var 1
-#pragma unroll
-      for (int i = 0; i < NQ; ++i) {
-        const int s = base + i * PX;
-        tend[0 * VS + s] += acc[i][0];
-        tend[2 * VS + s] += acc[i][1];
-        tend[3 * VS + s] += acc[i][2];
-        tend[1 * VS + s] += acc[i][3];
-        tend[4 * VS + s] += acc[i][4];
-      }
-    }
-    __syncthreads();
-  }
-
-  // ---- phase C: x and y faces, thread per face node ------------------------
-  // The neighbour state of face lf+1 is fetched while face lf is evaluated.
+  // Neighbour state of face lf, fetched one face ahead of its use so the
+  // (mostly L2-resident) gather hides behind arithmetic.
   NbrRaw<Real> cur, nxt;
   auto fetch = [&](int lf, NbrRaw<Real>& r) {
     const int dir = lf >> 1, side = lf & 1;
@@ -388,14 +345,66 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
       r.ph = P.ghost_phi[g * N2 + l];
     }
   };
-  if (SURF) {
+
+  // ---- phase B: x and y sweeps, results through shared memory -------------
+  if (VOL) {
+    if (active) {
+      Real acc[NQ][5];
+#pragma unroll
+      for (int i = 0; i < NQ; ++i)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
+      const int base = e * N3P + PX * l; // x line through (y, z) = (l0, l1)
+      sweep_line<Real, NQ, 0>(P, vals, VS, base, 1, acc);
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) {
+        const int s = base + i;
+        tend[0 * VS + s] = acc[i][0];
+        tend[1 * VS + s] = acc[i][1];
+        tend[2 * VS + s] = acc[i][2];
+        tend[3 * VS + s] = acc[i][3];
+        tend[4 * VS + s] = acc[i][4];
+      }
+    }
+    __syncthreads();
+    if (SURF && active) fetch(0, cur); // lands while the y sweep runs
+    if (active) {
+      Real acc[NQ][5];
+#pragma unroll
+      for (int i = 0; i < NQ; ++i)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
+      const int base = e * N3P + l0 + ZS * l1; // y line through (x, z) = (l0, l1)
+      sweep_line<Real, NQ, 1>(P, vals, VS, base, PX, acc);
+      // rotated frame of y: normal -> var 2, t1 = z -> var 3, t2 = x -> var 1
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) {
+        const int s = base + i * PX;
+        tend[0 * VS + s] += acc[i][0];
+        tend[2 * VS + s] += acc[i][1];
+        tend[3 * VS + s] += acc[i][2];
+        tend[1 * VS + s] += acc[i][3];
+        tend[4 * VS + s] += acc[i][4];
+      }
+    }
+    __syncthreads();
+  } else if (SURF) {
     if (active) fetch(0, cur);
+  }
+
+  // ---- phase C: the six faces, thread per face node -----------------------
+  // x and y faces update the shared slab; the z faces belong to the thread's
+  // own z line and go to registers (zf) for the commit.
+  Real zf[2][5];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) zf[0][v] = zf[1][v] = Real(0);
+  if (SURF) {
 #pragma unroll 1
-    for (int lf = 0; lf < 4; ++lf) {
+    for (int lf = 0; lf < 6; ++lf) {
       if (active) {
-        fetch(lf + 1, nxt);
+        if (lf < 5) fetch(lf + 1, nxt);
         const int dir = lf >> 1, side = lf & 1;
-        const int d1 = dir + 1;              // dir is 0 or 1 here
+        const int d1 = dir == 2 ? 0 : dir + 1;
         const int d2 = d1 == 2 ? 0 : d1 + 1;
         // FaceIndexer::node (mesh.hpp:107-114): tangential axes d1, d2
         const int s_own = e * N3P + (side ? NQ - 1 : 0) * spitch(dir) +
@@ -403,19 +412,27 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         const Node<Real> own = load_node(vals, VS, s_own, dir);
         Real c[5];
         face_contribution<Real, NQ>(P, own, cur, dir, side, eg, l, c);
-        tend[s_own] -= c[0];
-        tend[(1 + dir) * VS + s_own] -= c[1];
-        tend[(1 + d1) * VS + s_own] -= c[2];
-        tend[(1 + d2) * VS + s_own] -= c[3];
-        tend[4 * VS + s_own] -= c[4];
+        if (dir < 2) {
+          tend[s_own] -= c[0];
+          tend[(1 + dir) * VS + s_own] -= c[1];
+          tend[(1 + d1) * VS + s_own] -= c[2];
+          tend[(1 + d2) * VS + s_own] -= c[3];
+          tend[4 * VS + s_own] -= c[4];
+        } else {
+#pragma unroll
+          for (int v = 0; v < 5; ++v) {
+            if (side == 0) zf[0][v] = c[v];
+            else zf[1][v] = c[v];
+          }
+        }
         cur = nxt;
       }
       // the two faces of a direction share no node; the next direction does
-      if (lf & 1) __syncthreads();
+      if (lf == 1 || lf == 3) __syncthreads();
     }
   }
 
-  // ---- z faces, z sweep and commit: all on the thread's own z line ---------
+  // ---- z sweep and commit: all on the thread's own z line ------------------
   if (active) {
     Real acc[NQ][5]; // rotated frame of z: normal -> var 3, t1 = x -> 1, t2 = y -> 2
 #pragma unroll
@@ -423,20 +440,10 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
 #pragma unroll
       for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
     if (SURF) {
-      fetch(5, nxt);
-      {
-        const Node<Real> own = load_node(vals, VS, zbase, 2);
-        Real c[5];
-        face_contribution<Real, NQ>(P, own, cur, 2, 0, eg, l, c);
 #pragma unroll
-        for (int v = 0; v < 5; ++v) acc[0][v] -= c[v];
-      }
-      {
-        const Node<Real> own = load_node(vals, VS, zbase + (NQ - 1) * ZS, 2);
-        Real c[5];
-        face_contribution<Real, NQ>(P, own, nxt, 2, 1, eg, l, c);
-#pragma unroll
-        for (int v = 0; v < 5; ++v) acc[NQ - 1][v] -= c[v];
+      for (int v = 0; v < 5; ++v) {
+        acc[0][v] = -zf[0][v];
+        acc[NQ - 1][v] = acc[NQ - 1][v] - zf[1][v];
       }
     }
     if (VOL) sweep_line<Real, NQ, 2>(P, vals, VS, zbase, ZS, acc);
@@ -467,13 +474,24 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           val[1] = val[1] + f * qe[2 * N3];
           val[2] = val[2] + (-f) * qe[1 * N3];
         }
+        Real knew[5];
         if (P.a_old == Real(0)) {
 #pragma unroll
-          for (int v = 0; v < 5; ++v) oe[v * N3 + k * N2] = P.a_new * val[v];
+          for (int v = 0; v < 5; ++v) knew[v] = P.a_new * val[v];
         } else {
 #pragma unroll
-          for (int v = 0; v < 5; ++v)
-            oe[v * N3 + k * N2] = P.a_old * ov[k][v] + P.a_new * val[v];
+          for (int v = 0; v < 5; ++v) knew[v] = P.a_old * ov[k][v] + P.a_new * val[v];
+        }
+#pragma unroll
+        for (int v = 0; v < 5; ++v) oe[v * N3 + k * N2] = knew[v];
+        if (P.q_next != nullptr) {
+          // LSRK register update folded into the same pass (Solver::axpy,
+          // solver.hpp:342-353): q_next = q + b k. q is double buffered
+          // because neighbouring CTAs still read this element's faces.
+          const Real* qe = P.q + eg * (5 * N3) + l + k * N2;
+          Real* qn = P.q_next + eg * (5 * N3) + l + k * N2;
+#pragma unroll
+          for (int v = 0; v < 5; ++v) qn[v * N3] = qe[v * N3] + P.b_upd * knew[v];
         }
       } else {
 #pragma unroll

@@ -257,7 +257,8 @@ int SolverCore::build_shard(LocalShard& ls) {
 }
 
 int SolverCore::set_path(int path) {
-  if (path != ESDG_B200_PATH_SPLIT && path != ESDG_B200_PATH_FUSED) {
+  if (path != ESDG_B200_PATH_SPLIT && path != ESDG_B200_PATH_FUSED &&
+      path != ESDG_B200_PATH_STAGE) {
     set_message("set_path: unknown path");
     return ESDG_B200_BADARG;
   }
@@ -498,7 +499,7 @@ int SolverCore::rhs(int src, int dst, double a_old, double a_new,
   const bool halo = any_halo_ && !volume_only;
   const int source = (with_source && opt_.settings.coriolis_mode != 0) ? 1 : 0;
   if (halo) RC(exchange_begin(src));
-  if (path_ == ESDG_B200_PATH_FUSED && !volume_only) {
+  if (path_ != ESDG_B200_PATH_SPLIT && !volume_only) {
     if (halo) RC(exchange_end());
     for (auto& ls : shards_) {
       RC(timed(ls, kClsVolume, [&] {
@@ -528,6 +529,25 @@ int SolverCore::rhs(int src, int dst, double a_old, double a_new,
   return ESDG_B200_OK;
 }
 
+// One LSRK stage in one kernel per partition: k <- a k + dt RHS(q), q <- q + b k
+int SolverCore::stage_fused(double a_old, double a_new, double b, int stage) {
+  const bool halo = any_halo_;
+  if (halo) {
+    RC(exchange_begin(ESDG_B200_REG_Q));
+    RC(exchange_end());
+  }
+  for (auto& ls : shards_) {
+    RC(timed(ls, kClsVolume, [&] {
+      return ls.dev->stage_fused(a_old, a_new, b, opt_.settings.coriolis_mode != 0 ? 1 : 0, stage, nullptr);
+    }));
+    if (halo && !ls.halo.peers.empty()) {
+      CU(cudaSetDevice(ls.dev->device()));
+      CU(cudaEventRecord(ls.ev_surf, ls.dev->stream()));
+    }
+  }
+  return ESDG_B200_OK;
+}
+
 int SolverCore::axpy(double b) {
   for (auto& ls : shards_)
     RC(timed(ls, kClsUpdate, [&] { return ls.dev->axpy(b, nullptr); }));
@@ -542,8 +562,12 @@ int SolverCore::step(double dt, bool do_check) {
   for (int s = 0; s < 5; ++s) {
     const double as = opt_.precision == 8 ? a[s] : double(float(a[s]));
     const double bs = opt_.precision == 8 ? b[s] : double(float(b[s]));
-    RC(rhs(ESDG_B200_REG_Q, ESDG_B200_REG_K, as, dt, true, false, s));
-    RC(axpy(bs));
+    if (path_ == ESDG_B200_PATH_STAGE) {
+      RC(stage_fused(as, dt, bs, s));
+    } else {
+      RC(rhs(ESDG_B200_REG_Q, ESDG_B200_REG_K, as, dt, true, false, s));
+      RC(axpy(bs));
+    }
   }
   if (do_check) return check();
   return ESDG_B200_OK;

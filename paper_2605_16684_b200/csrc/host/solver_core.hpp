@@ -61,6 +61,7 @@ public:
                         bool volume_only);
   int rhs(int src, int dst, double a_old, double a_new, bool with_source,
           bool volume_only, int stage);
+  int stage_fused(double a_old, double a_new, double b, int stage);
   int axpy(double b);
   int step(double dt, bool check);
   int sync();

@@ -2,6 +2,7 @@
 // (include/esdg_b200.h, "shard" entry points). Owns device memory, derives
 // the kernel constants exactly like the reference's Operators<Real>
 // (core/include/esdg/kernels.hpp:70-92) and launches K1-K5.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -191,13 +192,30 @@ public:
           int with_source, int stage, cudaStream_t st) override {
     if ((src != 0 && src != 1) || (dst != 0 && dst != 1) || src == dst)
       return bad("rhs: src and dst must be distinct registers 0/1");
+    return launch(mode, src, dst, a_old, a_new, 0.0, nullptr, with_source, stage, st);
+  }
+
+  int stage_fused(double a_old, double a_new, double b, int with_source, int stage,
+                  cudaStream_t st) override {
+    CU(cudaSetDevice(device_));
+    if (!q_alt_) {
+      const size_t state_bytes = sizeof(Real) * size_t(ne_) * 5 * size_t(n3_);
+      CU(cudaMalloc(&q_alt_, state_bytes ? state_bytes : 16));
+    }
+    const int rc = launch(kModeFused, 0, 1, a_old, a_new, b, q_alt_, with_source, stage, st);
+    if (rc == ESDG_B200_OK) std::swap(q_, q_alt_); // the new state is current
+    return rc;
+  }
+
+  int launch(int mode, int src, int dst, double a_old, double a_new, double b,
+             Real* q_next, int with_source, int stage, cudaStream_t st) {
     CU(cudaSetDevice(device_));
     cudaError_t e = cudaErrorInvalidValue;
     switch (nq_) {
 #define ESDG_CASE(NQ)                                                          \
   case NQ:                                                                     \
-    e = run_rhs<NQ>(mode, src, dst, a_old, a_new, with_source, stage,          \
-                    pick(st));                                                 \
+    e = run_rhs<NQ>(mode, src, dst, a_old, a_new, b, q_next, with_source,      \
+                    stage, pick(st));                                          \
     break;
       ESDG_CASE(2) ESDG_CASE(3) ESDG_CASE(4) ESDG_CASE(5) ESDG_CASE(6)
       ESDG_CASE(7) ESDG_CASE(8)
@@ -274,9 +292,12 @@ public:
 private:
   template <int NQ>
   cudaError_t run_rhs(int mode, int src, int dst, double a_old, double a_new,
-                      int with_source, int stage, cudaStream_t st) {
+                      double b, Real* q_next, int with_source, int stage,
+                      cudaStream_t st) {
     dev::RhsParams<Real, NQ> P;
     P.q = reg_ptr(src);
+    P.q_next = q_next;
+    P.b_upd = Real(b);
     P.out = reg_ptr(dst);
     P.phi = phi_;
     P.nbr = nbr_;
@@ -327,6 +348,7 @@ private:
   void release() {
     if (device_ >= 0) cudaSetDevice(device_);
     cudaFree(q_);
+    cudaFree(q_alt_);
     cudaFree(k_);
     cudaFree(phi_);
     cudaFree(nbr_);
@@ -349,7 +371,7 @@ private:
   Real metric_[3] = {0, 0, 0}, lift_[3] = {0, 0, 0};
   std::vector<Real> negc_;
   dev::GasParams<Real> gas_{};
-  Real *q_ = nullptr, *k_ = nullptr, *phi_ = nullptr, *ghost_phi_ = nullptr;
+  Real *q_ = nullptr, *q_alt_ = nullptr, *k_ = nullptr, *phi_ = nullptr, *ghost_phi_ = nullptr;
   Real *recv_ = nullptr, *send_ = nullptr, *cor_f_ = nullptr;
   int32_t *nbr_ = nullptr, *send_elem_ = nullptr, *send_face_ = nullptr,
           *ylevel_ = nullptr;
@@ -619,6 +641,13 @@ int esdg_b200_shard_rhs_fused(esdg_b200_shard* s, int src, int dst,
   s->last_src = src;
   return s->impl->rhs(esdg_b200::kModeFused, src, dst, a_old, a_new, 1, stage,
                       cudaStream_t(stream));
+}
+
+int esdg_b200_shard_stage_fused(esdg_b200_shard* s, double a_old, double a_new,
+                                double b, int stage, void* stream) {
+  if (!s) return ESDG_B200_BADARG;
+  s->last_src = ESDG_B200_REG_Q;
+  return s->impl->stage_fused(a_old, a_new, b, 1, stage, cudaStream_t(stream));
 }
 
 int esdg_b200_shard_axpy(esdg_b200_shard* s, double b, void* stream) {

@@ -33,6 +33,9 @@ public:
   // mode: RhsMode (esdg_launch.hpp)
   virtual int rhs(int mode, int src, int dst, double a_old, double a_new,
                   int with_source, int stage, cudaStream_t st) = 0;
+  // k <- a_old k + a_new RHS(q); q <- q + b k in one kernel (q double buffered)
+  virtual int stage_fused(double a_old, double a_new, double b, int with_source,
+                          int stage, cudaStream_t st) = 0;
   virtual int axpy(double b, cudaStream_t st) = 0;
   virtual int check(cudaStream_t st, int src, esdg_b200_error* err) = 0;
 };

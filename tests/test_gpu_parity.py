@@ -163,12 +163,13 @@ def test_partition_bitwise_rhs(port, ranks, path):
     assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("path", [capi.PATH_SPLIT, capi.PATH_STAGE])
 @pytest.mark.parametrize("ranks", [2, 4])
-def test_partition_bitwise_trajectory(port, ranks):
+def test_partition_bitwise_trajectory(port, ranks, path):
     """test_partition.cpp:94-100: 10 steps, order 3, bubble_mesh(1)."""
     states = []
     for r in (1, ranks):
-        o, g = make(port, "bubble", (1, False), 3, ranks=r)
+        o, g = make(port, "bubble", (1, False), 3, ranks=r, path=path)
         q = o.init_case(po.CASE_BUBBLE_SHARP).copy()
         g.set_state(q)
         dt = o.compute_dt(0.5)
@@ -178,7 +179,7 @@ def test_partition_bitwise_trajectory(port, ranks):
     assert np.array_equal(states[0], states[1])
 
 
-@pytest.mark.parametrize("path", [capi.PATH_SPLIT, capi.PATH_FUSED])
+@pytest.mark.parametrize("path", [capi.PATH_SPLIT, capi.PATH_FUSED, capi.PATH_STAGE])
 def test_trajectory_config1(port, path):
     """BASELINE.json configs[0]: 10 RK steps of the sharp bubble, N=4, 8^3.
     Tolerance: rho, E to 1e-12 of max|q_v|; momenta are
@@ -217,9 +218,10 @@ def test_rhs_fp32(port, order, case, seed, path):
     assert scaled_error(got, want, o.flux_scale(q)) <= TOL32
 
 
-def test_trajectory_fp32(port):
+@pytest.mark.parametrize("path", [capi.PATH_SPLIT, capi.PATH_STAGE])
+def test_trajectory_fp32(port, path):
     """FP32 10-step state within 1e-4 of max|q_v|."""
-    o, g = make(port, "bubble", (2, False), 4, prec="f32")
+    o, g = make(port, "bubble", (2, False), 4, prec="f32", path=path)
     q = o.init_case(po.CASE_BUBBLE_SHARP).copy()
     g.set_state(q)
     dt = o.compute_dt(0.5)
@@ -279,6 +281,21 @@ def test_diagnostics_match_oracle(port):
     g.rhs(0.0, 1.0)
     k = g.get_state(capi.REG_K)
     assert g.entropy_production() == o.entropy_production(q, k)
+
+
+def test_stage_path_equals_fused_plus_axpy_bitwise(port):
+    """The one-kernel-per-stage path performs the same operations as K1+K2
+    followed by K3, so trajectories are bitwise equal; state and k register
+    stay addressable through REG_Q / REG_K although q is double buffered."""
+    res = []
+    for path in (capi.PATH_FUSED, capi.PATH_STAGE):
+        o, g = make(port, "bubble", (1, True), 4, path=path, cor=(2, 1e-4, 1.6e-11, 0.0))
+        g.set_state(o.init_case(po.CASE_ENTROPY_TEST, 17).copy())
+        for _ in range(3):
+            g.step(2e-3)
+        res.append((g.get_state(capi.REG_Q), g.get_state(capi.REG_K)))
+    assert np.array_equal(res[0][0], res[1][0])
+    assert np.array_equal(res[0][1], res[1][1])
 
 
 def test_axpy_and_lsrk_pieces(port):

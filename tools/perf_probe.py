@@ -28,7 +28,7 @@ ne, n3 = mesh.ne, s.n3
 dof = ne * n3
 out.update(elements=ne, dof=dof, order=args.order, precision=args.precision)
 dt = 1e-3
-for path, name in ((capi.PATH_SPLIT, "split"), (capi.PATH_FUSED, "fused")):
+for path, name in ((capi.PATH_SPLIT, "split"), (capi.PATH_FUSED, "fused"), (capi.PATH_STAGE, "stage")):
     s.set_path(path)
     s.step(dt)          # warm-up
     s.sync()
