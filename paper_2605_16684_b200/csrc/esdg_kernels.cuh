@@ -286,6 +286,12 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   auto spitch = [](int ax) { return ax == 0 ? 1 : (ax == 1 ? PX : PX * NQ); };
   auto gpitch = [](int ax) { return ax == 0 ? 1 : (ax == 1 ? NQ : NQ * NQ); };
 
+  int codes[6] = {-1, -1, -1, -1, -1, -1};
+  if (SURF && active) {
+#pragma unroll
+    for (int lf = 0; lf < 6; ++lf) codes[lf] = P.nbr[eg * 6 + lf];
+  }
+
   // ---- phase A: primitives and logarithms, once per node ------------------
   // All global loads are issued before the first logarithm so they overlap.
   if (active) {
@@ -323,13 +329,15 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   __syncthreads();
 
   // Neighbour state of face lf, fetched one face ahead of its use so the
-  // (mostly L2-resident) gather hides behind arithmetic.
+  // (mostly L2-resident) gather hides behind arithmetic. The six neighbour
+  // codes were read at kernel start, so a fetch is one round trip, not two.
   NbrRaw<Real> cur, nxt;
   auto fetch = [&](int lf, NbrRaw<Real>& r) {
     const int dir = lf >> 1, side = lf & 1;
     const int d1 = dir == 2 ? 0 : dir + 1;
     const int d2 = d1 == 2 ? 0 : d1 + 1;
-    r.code = P.nbr[eg * 6 + lf];
+    r.code = lf == 0 ? codes[0] : lf == 1 ? codes[1] : lf == 2 ? codes[2]
+             : lf == 3 ? codes[3] : lf == 4 ? codes[4] : codes[5];
     if (r.code >= 0) {
       // opposite side of the neighbour, same tangential (s, t)
       const int n_nb = (side ? 0 : NQ - 1) * gpitch(dir) + l0 * gpitch(d1) +
@@ -448,15 +456,35 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     }
     if (VOL) sweep_line<Real, NQ, 2>(P, vals, VS, zbase, ZS, acc);
 
-    // commit (solver.hpp:199-223), one z line per thread, coalesced over l
-    Real* oe = P.out + eg * (5 * N3) + l;
-    Real ov[NQ][5];
+    // commit (solver.hpp:199-223), one z line per thread, coalesced over l.
+    // Every global load of the commit is issued before its first store: the
+    // compiler cannot prove that out / q / q_next do not alias, so loads
+    // placed after a store would each wait out a full L2 round trip.
+    const Real* __restrict__ qe = P.q + eg * (5 * N3) + l;
+    Real* __restrict__ oe = P.out + eg * (5 * N3) + l;
+    const bool update = VOL && P.q_next != nullptr;
+    const bool source = VOL && P.with_source != 0;
+    Real ov[NQ][5], qv[NQ][5], cf = Real(0);
     if (read_out) {
 #pragma unroll
       for (int k = 0; k < NQ; ++k)
 #pragma unroll
         for (int v = 0; v < 5; ++v) ov[k][v] = oe[v * N3 + k * N2];
     }
+    if (update) {
+#pragma unroll
+      for (int k = 0; k < NQ; ++k)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) qv[k][v] = qe[v * N3 + k * N2];
+    } else if (source) {
+      // coriolis_source (physics.hpp:297-306) only needs the momenta
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) {
+        qv[k][1] = qe[1 * N3 + k * N2];
+        qv[k][2] = qe[2 * N3 + k * N2];
+      }
+    }
+    if (source) cf = P.cor_f[P.ylevel[eg] * NQ + l1];
 #pragma unroll
     for (int k = 0; k < NQ; ++k) {
       const int s = zbase + k * ZS;
@@ -467,12 +495,10 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
       val[3] = tend[3 * VS + s] + acc[k][1];
       val[4] = tend[4 * VS + s] + acc[k][4];
       if (VOL) {
-        if (P.with_source) {
-          // coriolis_source (physics.hpp:297-306): h = (0, f q2, -f q1, 0, 0)
-          const Real* qe = P.q + eg * (5 * N3) + l + k * N2;
-          const Real f = P.cor_f[P.ylevel[eg] * NQ + l1];
-          val[1] = val[1] + f * qe[2 * N3];
-          val[2] = val[2] + (-f) * qe[1 * N3];
+        if (source) {
+          // h = (0, f q2, -f q1, 0, 0)
+          val[1] = val[1] + cf * qv[k][2];
+          val[2] = val[2] + (-cf) * qv[k][1];
         }
         Real knew[5];
         if (P.a_old == Real(0)) {
@@ -484,14 +510,13 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         }
 #pragma unroll
         for (int v = 0; v < 5; ++v) oe[v * N3 + k * N2] = knew[v];
-        if (P.q_next != nullptr) {
+        if (update) {
           // LSRK register update folded into the same pass (Solver::axpy,
           // solver.hpp:342-353): q_next = q + b k. q is double buffered
           // because neighbouring CTAs still read this element's faces.
-          const Real* qe = P.q + eg * (5 * N3) + l + k * N2;
-          Real* qn = P.q_next + eg * (5 * N3) + l + k * N2;
+          Real* __restrict__ qn = P.q_next + eg * (5 * N3) + l + k * N2;
 #pragma unroll
-          for (int v = 0; v < 5; ++v) qn[v * N3] = qe[v * N3] + P.b_upd * knew[v];
+          for (int v = 0; v < 5; ++v) qn[v * N3] = qv[k][v] + P.b_upd * knew[v];
         }
       } else {
 #pragma unroll
