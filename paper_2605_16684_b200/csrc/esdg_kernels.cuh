@@ -59,6 +59,7 @@ struct RhsParams {
   GasParams<Real> gas;
   Real negc[3][NQ * NQ]; // -(2 g_d D_ij), kernels.hpp:187, 224-225
   Real lift[3];          // Operators::face_coef, kernels.hpp:86-88
+  int prefetch_ctas;     // resident CTAs chip-wide: L2 prefetch distance
   int with_source;       // Coriolis on (commit_volume, solver.hpp:205-216)
   int dissipation;
   int stage;
@@ -310,6 +311,19 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
       const int bytes = ne_blk * 5 * N3 * int(sizeof(Real));
       for (int off = tid * 128; off < bytes; off += EPB * N2 * 128)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(ob + off));
+    }
+    // ... and the q / phi slabs of the CTA that will follow this one on the
+    // SM (one resident wave ahead), so its phase A starts from L2, not HBM
+    {
+      const long long en = e0 + static_cast<long long>(P.prefetch_ctas) * EPB;
+      if (en + EPB <= P.ne) {
+        const char* qb = reinterpret_cast<const char*>(P.q + en * (5 * N3));
+        for (int off = tid * 128; off < EPB * 5 * N3 * int(sizeof(Real)); off += EPB * N2 * 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(qb + off));
+        const char* pb = reinterpret_cast<const char*>(P.phi + en * N3);
+        for (int off = tid * 128; off < EPB * N3 * int(sizeof(Real)); off += EPB * N2 * 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + off));
+      }
     }
 #pragma unroll
     for (int k = 0; k < NQ; ++k) {

@@ -62,6 +62,8 @@ public:
       return ESDG_B200_CUDA;
     }
     CU(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    sm_count_ = prop.multiProcessorCount;
+    smem_per_sm_ = prop.sharedMemPerMultiprocessor;
 
     // Operators<Real> (kernels.hpp:79-91): 64-bit operators rounded to Real
     std::vector<Real> D(static_cast<size_t>(n2_)), w(static_cast<size_t>(nq_));
@@ -318,6 +320,13 @@ private:
       P.lift[k] = lift_[k];
     }
     P.with_source = (with_source && coriolis_mode_ != 0) ? 1 : 0;
+    {
+      int threads = 0, epb = 0;
+      size_t smem = 0;
+      rhs_launch_shape<Real, NQ>(&threads, &epb, &smem);
+      const int per_sm = std::max(1, std::min(int(smem_per_sm_ / std::max<size_t>(smem, 1)), 2048 / std::max(threads, 1)));
+      P.prefetch_ctas = sm_count_ * per_sm;
+    }
     P.dissipation = dissipation_;
     P.stage = stage;
     return launch_rhs<Real, NQ>(mode, P, st);
@@ -365,7 +374,8 @@ private:
     if (stream_) cudaStreamDestroy(stream_);
   }
 
-  int nq_ = 0, n2_ = 0, n3_ = 0, device_ = -1;
+  int nq_ = 0, n2_ = 0, n3_ = 0, device_ = -1, sm_count_ = 148;
+  size_t smem_per_sm_ = 233472;
   int64_t ne_ = 0, elem_offset_ = 0, n_ghost_ = 0, n_send_ = 0;
   int dissipation_ = 1, coriolis_mode_ = 0;
   Real metric_[3] = {0, 0, 0}, lift_[3] = {0, 0, 0};
