@@ -336,27 +336,37 @@ def main_b200(args, rank, local_rank, world):
     w = work_model(nq, rb)
     per_launch = {k: timers[k] / n_rhs for k in ("volume", "surface", "update")}
     kernels = {}
-    if args.path == "fused":
+    upd_flops = 10 * nq ** 3          # q += b k: 2 flops per value
+    if args.path == "stage":
+        flops = (w["volume_flops"] + w["surface_flops"] + upd_flops) * n_local
+        dom = "rhs_kernel<VOL,SURF> + register update (K1+K2+K3, one launch per LSRK stage)"
+        dom_s = per_launch["volume"]
+        traffic_key = "stage"
+    elif args.path == "fused":
         flops = (w["volume_flops"] + w["surface_flops"]) * n_local
         dom = "rhs_kernel<VOL,SURF> (fused K1+K2)"
         dom_s = per_launch["volume"]
+        traffic_key = "fused"
     else:
         flops = w["volume_flops"] * n_local
         dom = "rhs_kernel<VOL> (K1 volume)"
         dom_s = per_launch["volume"]
+        traffic_key = "volume"
         surf_gbs = w["surface_bytes"] * n_local / per_launch["surface"] / 1e9
         kernels["surface"] = {"bound": "hbm", "achieved": surf_gbs, "peak": peaks["hbm_gbs"],
                               "unit": "GB/s", "frac": surf_gbs / peaks["hbm_gbs"],
                               "ms": 1e3 * per_launch["surface"]}
     achieved = flops / dom_s / 1e12
-    upd_gbs = w["update_bytes"] * n_local / per_launch["update"] / 1e9
-    kernels["update"] = {"bound": "hbm", "achieved": upd_gbs, "peak": peaks["hbm_gbs"],
-                         "unit": "GB/s", "frac": upd_gbs / peaks["hbm_gbs"],
-                         "ms": 1e3 * per_launch["update"]}
+    if per_launch["update"] > 0:
+        upd_gbs = w["update_bytes"] * n_local / per_launch["update"] / 1e9
+        kernels["update"] = {"bound": "hbm", "achieved": upd_gbs, "peak": peaks["hbm_gbs"],
+                             "unit": "GB/s", "frac": upd_gbs / peaks["hbm_gbs"],
+                             "ms": 1e3 * per_launch["update"]}
     roofline = {
         "kernel": dom, "bound": "fp64" if rb == 8 else "fp32",
         "achieved": achieved, "peak": fma_peak, "unit": "TFLOP/s", "frac": achieved / fma_peak,
-        "traffic": ncu_traffic("fused" if args.path == "fused" else "volume"),
+        "traffic": ncu_traffic(traffic_key) if (args.order == 4 and rb == 8 and args.refinement == 5
+                                                and world == 1 and args.case == "bubble") else None,
         "ms_per_launch": 1e3 * dom_s,
         "flops_model": "reference PerfRecord model (diagnostics.cpp:33-81): "
                        f"{flops // n_local} flops/element/launch",

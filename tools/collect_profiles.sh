@@ -1,0 +1,24 @@
+#!/bin/bash
+# Runs on the GPU box (via gpurun): bench lines, ncu launch list and ncu --set
+# full captures that profiles/ is built from. Output goes to gpurun_out/.
+set -u
+OUT=gpurun_out
+mkdir -p $OUT
+TAG=${1:-r1}
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem,power.draw,power.limit --format=csv > $OUT/${TAG}_smi.csv
+timeout 400 python bench.py > $OUT/${TAG}_bench_stage.json 2> $OUT/${TAG}_bench_stage.err
+timeout 300 python bench.py --path split --no-cpu-baseline > $OUT/${TAG}_bench_split.json 2> $OUT/${TAG}_bench_split.err
+timeout 300 python bench.py --path fused --no-cpu-baseline --no-e2e > $OUT/${TAG}_bench_fused.json 2> $OUT/${TAG}_bench_fused.err
+timeout 300 python bench.py --precision f32 --no-cpu-baseline > $OUT/${TAG}_bench_stage_f32.json 2> $OUT/${TAG}_bench_f32.err
+timeout 300 python bench.py --impl reference --steps 5 --warmup 1 > $OUT/${TAG}_bench_reference.json 2> $OUT/${TAG}_bench_reference.err
+# every launch of the default bench command with its device time
+timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
+  --log-file $OUT/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > $OUT/${TAG}_ncu_launches.log 2>&1
+timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
+  --log-file $OUT/${TAG}_launches_split.csv python bench.py --path split --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > $OUT/${TAG}_ncu_launches_split.log 2>&1
+# full captures at the bench size (configs[1]); one launch each
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:rhs_kernel -s 16 -c 1 \
+  -o $OUT/${TAG}_full_stage python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $OUT/${TAG}_ncu_full_stage.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"rhs_kernel|axpy_kernel" -s 45 -c 3 \
+  -o $OUT/${TAG}_full_split python bench.py --path split --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $OUT/${TAG}_ncu_full_split.log 2>&1
+ls -la $OUT | tail -30

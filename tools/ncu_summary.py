@@ -18,10 +18,6 @@ KEYS = [
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
     "lts__throughput.avg.pct_of_peak_sustained_elapsed",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
-    "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum",
-    "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
-    "smsp__sass_thread_inst_executed_op_ffma_pred_on.sum", "smsp__sass_thread_inst_executed_op_fmul_pred_on.sum",
-    "smsp__sass_thread_inst_executed_op_fadd_pred_on.sum",
 ]
 
 
@@ -48,13 +44,21 @@ def main():
             t = d.get("gpu__time_duration.sum")
             unit = units[idx["gpu__time_duration.sum"]]
             sec = t * {"ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0, "usecond": 1e-6, "msecond": 1e-3, "nsecond": 1e-9}.get(unit, 1e-9)
-            f64 = 2 * d.get("smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", 0) + \
-                d.get("smsp__sass_thread_inst_executed_op_dmul_pred_on.sum", 0) + \
-                d.get("smsp__sass_thread_inst_executed_op_dadd_pred_on.sum", 0)
-            f32 = 2 * d.get("smsp__sass_thread_inst_executed_op_ffma_pred_on.sum", 0) + \
-                d.get("smsp__sass_thread_inst_executed_op_fmul_pred_on.sum", 0) + \
-                d.get("smsp__sass_thread_inst_executed_op_fadd_pred_on.sum", 0)
-            print(f"  hardware-counted FLOP/s: fp64 {f64 / sec / 1e12:.2f} TF, fp32 {f32 / sec / 1e12:.2f} TF  (duration {sec * 1e3:.4f} ms)")
+            def per_cycle(op):
+                k = f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum.per_cycle_elapsed"
+                return float(r[idx[k]].replace(",", "")) if k in idx and r[idx[k]] not in ("", "n/a") else 0.0
+            cyc = float(r[idx["sm__cycles_elapsed.avg"]].replace(",", "")) if "sm__cycles_elapsed.avg" in idx else 0.0
+            dp = (per_cycle("dfma"), per_cycle("dmul"), per_cycle("dadd"))
+            sp = (per_cycle("ffma"), per_cycle("fmul"), per_cycle("fadd"))
+            f64 = (2 * dp[0] + dp[1] + dp[2]) * cyc
+            f32 = (2 * sp[0] + sp[1] + sp[2]) * cyc
+            print(f"  FP64 thread-instr/cycle (chip): dfma {dp[0]:.0f} dmul {dp[1]:.0f} dadd {dp[2]:.0f} "
+                  f"= {sum(dp):.0f} of 9472 issue slots ({sum(dp) / 9472:.1%})")
+            if sum(sp) > 0:
+                print(f"  FP32 thread-instr/cycle (chip): ffma {sp[0]:.0f} fmul {sp[1]:.0f} fadd {sp[2]:.0f} "
+                      f"= {sum(sp):.0f} of 18944 issue slots ({sum(sp) / 18944:.1%})")
+            print(f"  hardware-counted FLOP/s: fp64 {f64 / sec / 1e12:.2f} TF, fp32 {f32 / sec / 1e12:.2f} TF  "
+                  f"(duration {sec * 1e3:.4f} ms, {cyc:.0f} SM cycles)")
 
 
 if __name__ == "__main__":
