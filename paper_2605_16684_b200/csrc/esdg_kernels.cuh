@@ -147,24 +147,26 @@ __device__ __forceinline__ Node<Real> rotate_node(const Real nv[V_COUNT],
   return n;
 }
 
-// One line sweep of the flux-differenced volume term in direction DIR
+// One line sweep of the flux-differenced volume term in direction `dir`
 // (sweep_direction, kernels.hpp:154-249): pulls the NQ nodes of a line into
 // registers, ADDS the diagonal point fluxes and every unordered pair (once)
-// to acc, which lives in the rotated frame of DIR.
-template <class Real, int NQ, int DIR>
+// to acc, which lives in the rotated frame of `dir`. One code instance
+// serves the three directions (the instruction cache is a real constraint
+// for these fully unrolled bodies).
+template <class Real, int NQ>
 __device__ __forceinline__ void sweep_line(const RhsParams<Real, NQ>& P,
                                            const Real* vals, int VS, int base,
-                                           int stride, Real (&acc)[NQ][5]) {
+                                           int stride, int dir, Real (&acc)[NQ][5]) {
   Node<Real> nd[NQ];
 #pragma unroll
-  for (int i = 0; i < NQ; ++i) nd[i] = load_node(vals, VS, base + i * stride, DIR);
+  for (int i = 0; i < NQ; ++i) nd[i] = load_node(vals, VS, base + i * stride, dir);
   // diagonal: t_i -= 2 g_d D_ii F(q_i, q_i)  (kernels.hpp:170-188). D_ii
   // vanishes analytically at interior LGL nodes; the host flushes its
   // O(1e-16) round-off residue to zero (shard.cu), so only the two end nodes
   // pay for a point flux here.
 #pragma unroll
   for (int i = 0; i < NQ; ++i) {
-    const Real cii = P.negc[DIR][i * NQ + i];
+    const Real cii = P.negc[dir][i * NQ + i];
     if (cii != Real(0)) {
       Real f[5];
       point_flux(nd[i], P.gas.cg, f);
@@ -179,8 +181,8 @@ __device__ __forceinline__ void sweep_line(const RhsParams<Real, NQ>& P,
     for (int j = 0; j < NQ; ++j) {
       if (j <= i) continue; // constant bounds keep the unroll total
       const PairFlux<Real> pf = pair_flux(nd[i], nd[j], P.gas.cg);
-      const Real cij = P.negc[DIR][i * NQ + j];
-      const Real cji = P.negc[DIR][j * NQ + i];
+      const Real cij = P.negc[dir][i * NQ + j];
+      const Real cji = P.negc[dir][j * NQ + i];
       const Real fni = fma_(pf.tg, nd[i].hib, pf.f[1]);
       const Real fnj = fma_(-pf.tg, nd[j].hib, pf.f[1]);
       acc[i][0] = fma_(cij, pf.f[0], acc[i][0]);
@@ -293,6 +295,32 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     for (int lf = 0; lf < 6; ++lf) codes[lf] = P.nbr[eg * 6 + lf];
   }
 
+  // Neighbour state of face lf, fetched one face ahead of its use so the
+  // (mostly L2-resident) gather hides behind arithmetic. The six neighbour
+  // codes were read at kernel start, so a fetch is one round trip, not two.
+  NbrRaw<Real> cur, nxt;
+  auto fetch = [&](int lf, NbrRaw<Real>& r) {
+    const int dir = lf >> 1, side = lf & 1;
+    const int d1 = dir == 2 ? 0 : dir + 1;
+    const int d2 = d1 == 2 ? 0 : d1 + 1;
+    r.code = lf == 0 ? codes[0] : lf == 1 ? codes[1] : lf == 2 ? codes[2]
+             : lf == 3 ? codes[3] : lf == 4 ? codes[4] : codes[5];
+    if (r.code >= 0) {
+      // opposite side of the neighbour, same tangential (s, t)
+      const int n_nb = (side ? 0 : NQ - 1) * gpitch(dir) + l0 * gpitch(d1) +
+                       l1 * gpitch(d2);
+      const Real* qn = P.q + static_cast<long long>(r.code) * (5 * N3);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) r.q[v] = qn[v * N3 + n_nb];
+      r.ph = P.phi[static_cast<long long>(r.code) * N3 + n_nb];
+    } else if (r.code <= -2) {
+      const long long g = (-2 - r.code) >> 1;
+#pragma unroll
+      for (int v = 0; v < 5; ++v) r.q[v] = P.ghost_q[(g * 5 + v) * N2 + l];
+      r.ph = P.ghost_phi[g * N2 + l];
+    }
+  };
+
   // ---- phase A: primitives and logarithms, once per node ------------------
   // All global loads are issued before the first logarithm so they overlap.
   if (active) {
@@ -325,6 +353,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + off));
       }
     }
+    if (SURF) fetch(0, cur); // first face's neighbour trace: lands during the logs
 #pragma unroll
     for (int k = 0; k < NQ; ++k) {
       Real nv[V_COUNT], pr;
@@ -334,92 +363,16 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
       const int s = zbase + k * ZS;
 #pragma unroll
       for (int j = 0; j < V_COUNT; ++j) vals[j * VS + s] = nv[j];
-      if (!VOL) {
 #pragma unroll
-        for (int v = 0; v < 5; ++v) tend[v * VS + s] = Real(0);
-      }
+      for (int v = 0; v < 5; ++v) tend[v * VS + s] = Real(0);
     }
   }
   __syncthreads();
 
-  // Neighbour state of face lf, fetched one face ahead of its use so the
-  // (mostly L2-resident) gather hides behind arithmetic. The six neighbour
-  // codes were read at kernel start, so a fetch is one round trip, not two.
-  NbrRaw<Real> cur, nxt;
-  auto fetch = [&](int lf, NbrRaw<Real>& r) {
-    const int dir = lf >> 1, side = lf & 1;
-    const int d1 = dir == 2 ? 0 : dir + 1;
-    const int d2 = d1 == 2 ? 0 : d1 + 1;
-    r.code = lf == 0 ? codes[0] : lf == 1 ? codes[1] : lf == 2 ? codes[2]
-             : lf == 3 ? codes[3] : lf == 4 ? codes[4] : codes[5];
-    if (r.code >= 0) {
-      // opposite side of the neighbour, same tangential (s, t)
-      const int n_nb = (side ? 0 : NQ - 1) * gpitch(dir) + l0 * gpitch(d1) +
-                       l1 * gpitch(d2);
-      const Real* qn = P.q + static_cast<long long>(r.code) * (5 * N3);
-#pragma unroll
-      for (int v = 0; v < 5; ++v) r.q[v] = qn[v * N3 + n_nb];
-      r.ph = P.phi[static_cast<long long>(r.code) * N3 + n_nb];
-    } else if (r.code <= -2) {
-      const long long g = (-2 - r.code) >> 1;
-#pragma unroll
-      for (int v = 0; v < 5; ++v) r.q[v] = P.ghost_q[(g * 5 + v) * N2 + l];
-      r.ph = P.ghost_phi[g * N2 + l];
-    }
-  };
-
-  // ---- phase B: x and y sweeps, results through shared memory -------------
-  if (VOL) {
-    if (active) {
-      Real acc[NQ][5];
-#pragma unroll
-      for (int i = 0; i < NQ; ++i)
-#pragma unroll
-        for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
-      const int base = e * N3P + PX * l; // x line through (y, z) = (l0, l1)
-      sweep_line<Real, NQ, 0>(P, vals, VS, base, 1, acc);
-#pragma unroll
-      for (int i = 0; i < NQ; ++i) {
-        const int s = base + i;
-        tend[0 * VS + s] = acc[i][0];
-        tend[1 * VS + s] = acc[i][1];
-        tend[2 * VS + s] = acc[i][2];
-        tend[3 * VS + s] = acc[i][3];
-        tend[4 * VS + s] = acc[i][4];
-      }
-    }
-    __syncthreads();
-    if (SURF && active) fetch(0, cur); // lands while the y sweep runs
-    if (active) {
-      Real acc[NQ][5];
-#pragma unroll
-      for (int i = 0; i < NQ; ++i)
-#pragma unroll
-        for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
-      const int base = e * N3P + l0 + ZS * l1; // y line through (x, z) = (l0, l1)
-      sweep_line<Real, NQ, 1>(P, vals, VS, base, PX, acc);
-      // rotated frame of y: normal -> var 2, t1 = z -> var 3, t2 = x -> var 1
-#pragma unroll
-      for (int i = 0; i < NQ; ++i) {
-        const int s = base + i * PX;
-        tend[0 * VS + s] += acc[i][0];
-        tend[2 * VS + s] += acc[i][1];
-        tend[3 * VS + s] += acc[i][2];
-        tend[1 * VS + s] += acc[i][3];
-        tend[4 * VS + s] += acc[i][4];
-      }
-    }
-    __syncthreads();
-  } else if (SURF) {
-    if (active) fetch(0, cur);
-  }
-
   // ---- phase C: the six faces, thread per face node -----------------------
-  // x and y faces update the shared slab; the z faces belong to the thread's
-  // own z line and go to registers (zf) for the commit.
-  Real zf[2][5];
-#pragma unroll
-  for (int v = 0; v < 5; ++v) zf[0][v] = zf[1][v] = Real(0);
+  // Every face subtracts its lift term from the shared tendency slab (zeroed
+  // by the z-line owners in phase A). Faces of one direction share no node,
+  // faces of different directions do (edges), hence the two barriers.
   if (SURF) {
 #pragma unroll 1
     for (int lf = 0; lf < 6; ++lf) {
@@ -434,42 +387,62 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         const Node<Real> own = load_node(vals, VS, s_own, dir);
         Real c[5];
         face_contribution<Real, NQ>(P, own, cur, dir, side, eg, l, c);
-        if (dir < 2) {
-          tend[s_own] -= c[0];
-          tend[(1 + dir) * VS + s_own] -= c[1];
-          tend[(1 + d1) * VS + s_own] -= c[2];
-          tend[(1 + d2) * VS + s_own] -= c[3];
-          tend[4 * VS + s_own] -= c[4];
-        } else {
-#pragma unroll
-          for (int v = 0; v < 5; ++v) {
-            if (side == 0) zf[0][v] = c[v];
-            else zf[1][v] = c[v];
-          }
-        }
+        tend[s_own] -= c[0];
+        tend[(1 + dir) * VS + s_own] -= c[1];
+        tend[(1 + d1) * VS + s_own] -= c[2];
+        tend[(1 + d2) * VS + s_own] -= c[3];
+        tend[4 * VS + s_own] -= c[4];
         cur = nxt;
       }
-      // the two faces of a direction share no node; the next direction does
-      if (lf == 1 || lf == 3) __syncthreads();
+      if (lf & 1) __syncthreads();
     }
   }
 
-  // ---- z sweep and commit: all on the thread's own z line ------------------
-  if (active) {
-    Real acc[NQ][5]; // rotated frame of z: normal -> var 3, t1 = x -> 1, t2 = y -> 2
+  // ---- phase B: the three line sweeps, one code instance -------------------
+  // x and y results are handed to the z-line owners through the shared slab;
+  // the z sweep stays in registers because the same thread commits that line.
+  Real acc[NQ][5];
 #pragma unroll
-    for (int i = 0; i < NQ; ++i)
+  for (int i = 0; i < NQ; ++i)
 #pragma unroll
-      for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
-    if (SURF) {
+    for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
+  if (VOL) {
+#pragma unroll 1
+    for (int dir = 0; dir < 3; ++dir) {
+      if (active) {
+        const int base = dir == 0 ? e * N3P + PX * l
+                                  : (dir == 1 ? e * N3P + l0 + ZS * l1 : zbase);
+        const int stride = dir == 0 ? 1 : (dir == 1 ? PX : ZS);
 #pragma unroll
-      for (int v = 0; v < 5; ++v) {
-        acc[0][v] = -zf[0][v];
-        acc[NQ - 1][v] = acc[NQ - 1][v] - zf[1][v];
+        for (int i = 0; i < NQ; ++i)
+#pragma unroll
+          for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
+        sweep_line<Real, NQ>(P, vals, VS, base, stride, dir, acc);
+        if (dir < 2) {
+          // un-rotate into the slab: normal -> 1+dir, then cyclic
+          const int d1 = dir + 1, d2 = dir == 0 ? 2 : 0;
+          Real* tn = tend + (1 + dir) * VS;
+          Real* tt1 = tend + (1 + d1) * VS;
+          Real* tt2 = tend + (1 + d2) * VS;
+          Real* t4 = tend + 4 * VS;
+#pragma unroll
+          for (int i = 0; i < NQ; ++i) {
+            const int s = base + i * stride;
+            tend[s] += acc[i][0];
+            tn[s] += acc[i][1];
+            tt1[s] += acc[i][2];
+            tt2[s] += acc[i][3];
+            t4[s] += acc[i][4];
+          }
+        }
       }
+      if (dir < 2) __syncthreads();
     }
-    if (VOL) sweep_line<Real, NQ, 2>(P, vals, VS, zbase, ZS, acc);
+  }
 
+  // ---- commit: slab (faces, x, y) + registers (z) on the thread's z line ---
+  if (active) {
+    // acc: rotated frame of z: normal -> var 3, t1 = x -> 1, t2 = y -> 2
     // commit (solver.hpp:199-223), one z line per thread, coalesced over l.
     // Every global load of the commit is issued before its first store: the
     // compiler cannot prove that out / q / q_next do not alias, so loads
