@@ -325,8 +325,12 @@ def main_b200(args, rank, local_rank, world):
                "call": "esdg_b200_solver_set_state + esdg_b200_solver_step + "
                        "esdg_b200_solver_get_state on pinned host StateField buffers"}
 
+    if exchange is not None:
+        halo_exchanges = exchange.exchanges
+        exchange.close()        # before the solver (and its stream) is destroyed
     if rank != 0:
         if world > 1:
+            del solver
             dist.destroy_process_group()
         return
 
@@ -402,7 +406,7 @@ def main_b200(args, rank, local_rank, world):
         "roofline": roofline, "cpu_baseline": cpu,
     }
     if exchange is not None:
-        line["config"]["halo_exchanges"] = exchange.exchanges
+        line["config"]["halo_exchanges"] = halo_exchanges
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -100,6 +100,20 @@ def reference_available(fast=False) -> bool:
     return os.path.exists(os.path.join(HERE, "_ref", "libesdg_ref_v3.so" if fast else "libesdg_ref.so"))
 
 
+class _Owned(np.ndarray):
+    """ndarray view of memory owned by a C handle; keeps the Python owner of
+    that handle alive for as long as the view (or any view of it) lives."""
+
+    def __array_finalize__(self, obj):
+        self._owner = getattr(obj, "_owner", None)
+
+
+def _owned(ptr, shape, owner):
+    a = np.ctypeslib.as_array(ptr, shape=shape).view(_Owned)
+    a._owner = owner
+    return a
+
+
 def _np_dtype(precision):
     return np.float64 if precision == "f64" else np.float32
 
@@ -347,17 +361,17 @@ class Solver:
     def state(self) -> np.ndarray:
         """Writable view of the internal q register, shape (ne, 5, n3)."""
         p = self._f("solver_state")(self.h)
-        return np.ctypeslib.as_array(p, shape=self.shape)
+        return _owned(p, self.shape, self)
 
     @property
     def kreg(self) -> np.ndarray:
         p = self._f("solver_kreg")(self.h)
-        return np.ctypeslib.as_array(p, shape=self.shape)
+        return _owned(p, self.shape, self)
 
     @property
     def phi(self) -> np.ndarray:
         p = self._f("solver_phi")(self.h)
-        return np.ctypeslib.as_array(p, shape=(self.ne, self.n3))
+        return _owned(p, (self.ne, self.n3), self)
 
     def ops(self):
         nq = self.nq

@@ -34,29 +34,57 @@ def device_tensor(ptr: int, count: int, dtype: torch.dtype, device: int) -> torc
 
 class HaloExchange:
     """peers: [(rank, offset, count)] in traces, identical for the send and the
-    receive buffer (esdg_b200_rank_halo); trace_len = 5 * nq^2 values."""
+    receive buffer (esdg_b200_rank_halo); trace_len = 5 * nq^2 values.
+
+    With a backend that cannot move device memory (gloo) and CUDA buffers the
+    blocks are staged through pinned host memory -- the reference's own
+    "host-staging model" (exchange.hpp:20-22); over NCCL they move directly
+    between the GPUs' buffers."""
 
     def __init__(self, peers, trace_len, send: torch.Tensor, recv: torch.Tensor, group=None):
         self.peers, self.trace_len = peers, trace_len
         self.send, self.recv, self.group = send, recv, group
         self.reqs = []
         self.exchanges = 0
+        self.h_send = self.h_recv = None
+        self.staged = send.is_cuda and dist.get_backend(group) == "gloo"
+        if self.staged:
+            self.h_send = torch.empty(send.shape, dtype=send.dtype, pin_memory=True)
+            self.h_recv = torch.empty(recv.shape, dtype=recv.dtype, pin_memory=True)
 
     def begin(self):
         """Posts all sends/receives of this RHS; returns immediately."""
+        src, dst = self.send, self.recv
+        if self.staged:
+            self.h_send.copy_(self.send, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            src, dst = self.h_send, self.h_recv
         ops = []
         for rank, off, cnt in self.peers:
             a, b = off * self.trace_len, (off + cnt) * self.trace_len
-            ops.append(dist.P2POp(dist.irecv, self.recv[a:b], rank, self.group))
-            ops.append(dist.P2POp(dist.isend, self.send[a:b], rank, self.group))
+            ops.append(dist.P2POp(dist.irecv, dst[a:b], rank, self.group))
+            ops.append(dist.P2POp(dist.isend, src[a:b], rank, self.group))
         self.reqs = dist.batch_isend_irecv(ops) if ops else []
         self.exchanges += 1
+
+    def close(self):
+        """Drops every tensor that references the solver's buffers or stream.
+        Must run BEFORE the solver is destroyed: torch's pinned-memory
+        allocator records an event on each stream a block was used on when the
+        block is freed, and the solver's stream dies with the solver."""
+        if self.send is not None and self.send.is_cuda:
+            torch.cuda.synchronize()
+        self.send = self.recv = None
+        self.h_send = self.h_recv = None
+        self.reqs = []
 
     def end(self):
         """Makes the current stream (CUDA) or the host (CPU) wait for them."""
         for r in self.reqs:
             r.wait()
         self.reqs = []
+        if self.staged:
+            self.recv.copy_(self.h_recv, non_blocking=True)
 
 
 def make_exchange_callback(solver, device: int, group=None):

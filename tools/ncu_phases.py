@@ -9,10 +9,22 @@ import io
 rep = sys.argv[1]
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
-# first line: kernel name; second: header
-hdr = rows[1]
+# the page holds one block per kernel: a "Kernel Name" line, a header line, rows
+want = sys.argv[2] if len(sys.argv) > 2 else None
+blocks, cur_name = [], None
+for r in rows:
+    if r and r[0] == "Kernel Name":
+        cur_name = r[1]
+        blocks.append([cur_name, None, []])
+    elif blocks and blocks[-1][1] is None:
+        blocks[-1][1] = r
+    elif blocks:
+        blocks[-1][2].append(r)
+blk = next((b for b in blocks if want is None or want in b[0]), blocks[0])
+print("kernel:", blk[0][:100])
+hdr = blk[1]
 idx = {h: i for i, h in enumerate(hdr)}
-data = rows[2:]
+data = blk[2]
 seg, segs = [], []
 for r in data:
     if len(r) < len(hdr):
