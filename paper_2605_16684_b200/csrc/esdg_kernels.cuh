@@ -163,16 +163,14 @@ __device__ __forceinline__ void sweep_line(const RhsParams<Real, NQ>& P,
   // diagonal: t_i -= 2 g_d D_ii F(q_i, q_i)  (kernels.hpp:170-188). D_ii
   // vanishes analytically at interior LGL nodes; the host flushes its
   // O(1e-16) round-off residue to zero (shard.cu), so only the two end nodes
-  // pay for a point flux here.
+  // carry a point flux -- known at compile time, no branch.
 #pragma unroll
-  for (int i = 0; i < NQ; ++i) {
+  for (int i = 0; i < NQ; i += NQ - 1) {
     const Real cii = P.negc[dir][i * NQ + i];
-    if (cii != Real(0)) {
-      Real f[5];
-      point_flux(nd[i], P.gas.cg, f);
+    Real f[5];
+    point_flux(nd[i], P.gas.cg, f);
 #pragma unroll
-      for (int v = 0; v < 5; ++v) acc[i][v] = fma_(cii, f[v], acc[i][v]);
-    }
+    for (int v = 0; v < 5; ++v) acc[i][v] = fma_(cii, f[v], acc[i][v]);
   }
   // off-diagonal pairs, each once (kernels.hpp:190-231)
 #pragma unroll
@@ -363,8 +361,11 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
       const int s = zbase + k * ZS;
 #pragma unroll
       for (int j = 0; j < V_COUNT; ++j) vals[j * VS + s] = nv[j];
+      if (SURF) {
+        // the faces are the slab's first writers and touch surface nodes only
 #pragma unroll
-      for (int v = 0; v < 5; ++v) tend[v * VS + s] = Real(0);
+        for (int v = 0; v < 5; ++v) tend[v * VS + s] = Real(0);
+      }
     }
   }
   __syncthreads();
@@ -419,20 +420,40 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
         sweep_line<Real, NQ>(P, vals, VS, base, stride, dir, acc);
         if (dir < 2) {
-          // un-rotate into the slab: normal -> 1+dir, then cyclic
+          // un-rotate into the slab: normal -> 1+dir, then cyclic. Without
+          // faces the x sweep is the slab's first writer and simply stores;
+          // otherwise all old values are fetched before the first store
+          // (one shared-memory round trip instead of 5 NQ dependent ones:
+          // the compiler cannot prove that the five arrays do not alias).
           const int d1 = dir + 1, d2 = dir == 0 ? 2 : 0;
           Real* tn = tend + (1 + dir) * VS;
           Real* tt1 = tend + (1 + d1) * VS;
           Real* tt2 = tend + (1 + d2) * VS;
           Real* t4 = tend + 4 * VS;
+          if (SURF || dir != 0) {
+            Real old[NQ][5];
+#pragma unroll
+            for (int i = 0; i < NQ; ++i) {
+              const int s = base + i * stride;
+              old[i][0] = tend[s];
+              old[i][1] = tn[s];
+              old[i][2] = tt1[s];
+              old[i][3] = tt2[s];
+              old[i][4] = t4[s];
+            }
+#pragma unroll
+            for (int i = 0; i < NQ; ++i)
+#pragma unroll
+              for (int v = 0; v < 5; ++v) acc[i][v] = old[i][v] + acc[i][v];
+          }
 #pragma unroll
           for (int i = 0; i < NQ; ++i) {
             const int s = base + i * stride;
-            tend[s] += acc[i][0];
-            tn[s] += acc[i][1];
-            tt1[s] += acc[i][2];
-            tt2[s] += acc[i][3];
-            t4[s] += acc[i][4];
+            tend[s] = acc[i][0];
+            tn[s] = acc[i][1];
+            tt1[s] = acc[i][2];
+            tt2[s] = acc[i][3];
+            t4[s] = acc[i][4];
           }
         }
       }
