@@ -320,7 +320,12 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   };
 
   // ---- phase A: primitives and logarithms, once per node ------------------
-  // All global loads are issued before the first logarithm so they overlap.
+  // All global loads -- the state, the geopotential and (accumulate form) the
+  // old contents of `out` -- are issued before the first logarithm, so the
+  // CTA pays for one HBM round trip. The slab starts as a_old * out_old and
+  // every later phase adds a_new * (its contribution); the commit then has
+  // no global load left to wait for.
+  const Real a_keep = VOL ? P.a_old : Real(1);
   if (active) {
     const Real* qe = P.q + eg * (5 * N3) + l;
     const Real* pe = P.phi + eg * N3 + l;
@@ -332,14 +337,26 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
       ph[k] = pe[k * N2];
     }
     if (read_out) {
-      // the commit reads this CTA's slab of `out` much later: pull it into L2
-      const char* ob = reinterpret_cast<const char*>(P.out + e0 * (5 * N3));
-      const int bytes = ne_blk * 5 * N3 * int(sizeof(Real));
-      for (int off = tid * 128; off < bytes; off += EPB * N2 * 128)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(ob + off));
+      const Real* oe = P.out + eg * (5 * N3) + l;
+      Real ov[NQ][5];
+#pragma unroll
+      for (int k = 0; k < NQ; ++k)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) ov[k][v] = oe[v * N3 + k * N2];
+#pragma unroll
+      for (int k = 0; k < NQ; ++k)
+#pragma unroll
+        for (int v = 0; v < 5; ++v)
+          tend[v * VS + zbase + k * ZS] = VOL ? a_keep * ov[k][v] : ov[k][v];
+    } else if (SURF) {
+      // the faces are the slab's first writers and touch surface nodes only
+#pragma unroll
+      for (int k = 0; k < NQ; ++k)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) tend[v * VS + zbase + k * ZS] = Real(0);
     }
-    // ... and the q / phi slabs of the CTA that will follow this one on the
-    // SM (one resident wave ahead), so its phase A starts from L2, not HBM
+    // the q / phi / out slabs of the CTA that will follow this one on the SM
+    // (one resident wave ahead), so its phase A starts from L2, not HBM
     {
       const long long en = e0 + static_cast<long long>(P.prefetch_ctas) * EPB;
       if (en + EPB <= P.ne) {
@@ -349,23 +366,35 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         const char* pb = reinterpret_cast<const char*>(P.phi + en * N3);
         for (int off = tid * 128; off < EPB * N3 * int(sizeof(Real)); off += EPB * N2 * 128)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + off));
+        if (read_out) {
+          const char* ob = reinterpret_cast<const char*>(P.out + en * (5 * N3));
+          for (int off = tid * 128; off < EPB * 5 * N3 * int(sizeof(Real)); off += EPB * N2 * 128)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(ob + off));
+        }
       }
     }
     if (SURF) fetch(0, cur); // first face's neighbour trace: lands during the logs
+    // The NQ nodes are independent: no branch separates them, so their
+    // reciprocal and logarithm chains interleave. A non-physical node is
+    // only remembered here and reported after the loop.
+    int bad = -1;
 #pragma unroll
     for (int k = 0; k < NQ; ++k) {
       Real nv[V_COUNT], pr;
-      if (!node_vals(qv[k], ph[k], P.gas.gm1, nv, pr))
-        raise_flag(P.flag, P.flag_records, P.stage, 0, P.elem_offset + eg, l + k * N2,
-                   double(qv[k][0]), double(pr));
+      const bool ok = node_vals(qv[k], ph[k], P.gas.gm1, nv, pr);
+      bad = (!ok && bad < 0) ? k : bad;
       const int s = zbase + k * ZS;
 #pragma unroll
       for (int j = 0; j < V_COUNT; ++j) vals[j * VS + s] = nv[j];
-      if (SURF) {
-        // the faces are the slab's first writers and touch surface nodes only
+    }
+    if (bad >= 0) {
+      const Real* qb = qe + bad * N2;
+      Real qq[5], nv[V_COUNT], pr;
 #pragma unroll
-        for (int v = 0; v < 5; ++v) tend[v * VS + s] = Real(0);
-      }
+      for (int v = 0; v < 5; ++v) qq[v] = qb[v * N3];
+      node_vals(qq, pe[bad * N2], P.gas.gm1, nv, pr);
+      raise_flag(P.flag, P.flag_records, P.stage, 0, P.elem_offset + eg, l + bad * N2,
+                 double(qq[0]), double(pr));
     }
   }
   __syncthreads();
@@ -388,11 +417,14 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         const Node<Real> own = load_node(vals, VS, s_own, dir);
         Real c[5];
         face_contribution<Real, NQ>(P, own, cur, dir, side, eg, l, c);
-        tend[s_own] -= c[0];
-        tend[(1 + dir) * VS + s_own] -= c[1];
-        tend[(1 + d1) * VS + s_own] -= c[2];
-        tend[(1 + d2) * VS + s_own] -= c[3];
-        tend[4 * VS + s_own] -= c[4];
+        const Real o0 = tend[s_own], o1 = tend[(1 + dir) * VS + s_own],
+                   o2 = tend[(1 + d1) * VS + s_own], o3 = tend[(1 + d2) * VS + s_own],
+                   o4 = tend[4 * VS + s_own];
+        tend[s_own] = fma_(-P.a_new, c[0], o0);
+        tend[(1 + dir) * VS + s_own] = fma_(-P.a_new, c[1], o1);
+        tend[(1 + d1) * VS + s_own] = fma_(-P.a_new, c[2], o2);
+        tend[(1 + d2) * VS + s_own] = fma_(-P.a_new, c[3], o3);
+        tend[4 * VS + s_own] = fma_(-P.a_new, c[4], o4);
         cur = nxt;
       }
       if (lf & 1) __syncthreads();
@@ -430,7 +462,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           Real* tt1 = tend + (1 + d1) * VS;
           Real* tt2 = tend + (1 + d2) * VS;
           Real* t4 = tend + 4 * VS;
-          if (SURF || dir != 0) {
+          if (SURF || dir != 0 || read_out) {
             Real old[NQ][5];
 #pragma unroll
             for (int i = 0; i < NQ; ++i) {
@@ -444,7 +476,12 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
 #pragma unroll
             for (int i = 0; i < NQ; ++i)
 #pragma unroll
-              for (int v = 0; v < 5; ++v) acc[i][v] = old[i][v] + acc[i][v];
+              for (int v = 0; v < 5; ++v) acc[i][v] = fma_(P.a_new, acc[i][v], old[i][v]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < NQ; ++i)
+#pragma unroll
+              for (int v = 0; v < 5; ++v) acc[i][v] = P.a_new * acc[i][v];
           }
 #pragma unroll
           for (int i = 0; i < NQ; ++i) {
@@ -461,24 +498,18 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     }
   }
 
-  // ---- commit: slab (faces, x, y) + registers (z) on the thread's z line ---
+  // ---- commit: slab (old out, faces, x, y) + registers (z) on the z line ----
   if (active) {
     // acc: rotated frame of z: normal -> var 3, t1 = x -> 1, t2 = y -> 2
     // commit (solver.hpp:199-223), one z line per thread, coalesced over l.
-    // Every global load of the commit is issued before its first store: the
-    // compiler cannot prove that out / q / q_next do not alias, so loads
-    // placed after a store would each wait out a full L2 round trip.
+    // Global loads (only the fused stage update and the Coriolis source need
+    // any) are issued before the first store: the compiler cannot prove that
+    // out / q / q_next do not alias.
     const Real* __restrict__ qe = P.q + eg * (5 * N3) + l;
     Real* __restrict__ oe = P.out + eg * (5 * N3) + l;
     const bool update = VOL && P.q_next != nullptr;
     const bool source = VOL && P.with_source != 0;
-    Real ov[NQ][5], qv[NQ][5], cf = Real(0);
-    if (read_out) {
-#pragma unroll
-      for (int k = 0; k < NQ; ++k)
-#pragma unroll
-        for (int v = 0; v < 5; ++v) ov[k][v] = oe[v * N3 + k * N2];
-    }
+    Real qv[NQ][5], cf = Real(0);
     if (update) {
 #pragma unroll
       for (int k = 0; k < NQ; ++k)
@@ -493,43 +524,45 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
       }
     }
     if (source) cf = P.cor_f[P.ylevel[eg] * NQ + l1];
+    Real knew[NQ][5];
 #pragma unroll
     for (int k = 0; k < NQ; ++k) {
       const int s = zbase + k * ZS;
-      Real val[5];
-      val[0] = tend[0 * VS + s] + acc[k][0];
-      val[1] = tend[1 * VS + s] + acc[k][2];
-      val[2] = tend[2 * VS + s] + acc[k][3];
-      val[3] = tend[3 * VS + s] + acc[k][1];
-      val[4] = tend[4 * VS + s] + acc[k][4];
-      if (VOL) {
-        if (source) {
-          // h = (0, f q2, -f q1, 0, 0)
-          val[1] = val[1] + cf * qv[k][2];
-          val[2] = val[2] + (-cf) * qv[k][1];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) knew[k][v] = tend[v * VS + s];
+    }
+    if (VOL) {
+      if (source) {
+        // h = (0, f q2, -f q1, 0, 0)
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) {
+          acc[k][2] = acc[k][2] + cf * qv[k][2];
+          acc[k][3] = acc[k][3] + (-cf) * qv[k][1];
         }
-        Real knew[5];
-        if (P.a_old == Real(0)) {
-#pragma unroll
-          for (int v = 0; v < 5; ++v) knew[v] = P.a_new * val[v];
-        } else {
-#pragma unroll
-          for (int v = 0; v < 5; ++v) knew[v] = P.a_old * ov[k][v] + P.a_new * val[v];
-        }
-#pragma unroll
-        for (int v = 0; v < 5; ++v) oe[v * N3 + k * N2] = knew[v];
-        if (update) {
-          // LSRK register update folded into the same pass (Solver::axpy,
-          // solver.hpp:342-353): q_next = q + b k. q is double buffered
-          // because neighbouring CTAs still read this element's faces.
-          Real* __restrict__ qn = P.q_next + eg * (5 * N3) + l + k * N2;
-#pragma unroll
-          for (int v = 0; v < 5; ++v) qn[v * N3] = qv[k][v] + P.b_upd * knew[v];
-        }
-      } else {
-#pragma unroll
-        for (int v = 0; v < 5; ++v) oe[v * N3 + k * N2] = ov[k][v] + P.a_new * val[v];
       }
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) {
+        knew[k][0] = fma_(P.a_new, acc[k][0], knew[k][0]);
+        knew[k][1] = fma_(P.a_new, acc[k][2], knew[k][1]);
+        knew[k][2] = fma_(P.a_new, acc[k][3], knew[k][2]);
+        knew[k][3] = fma_(P.a_new, acc[k][1], knew[k][3]);
+        knew[k][4] = fma_(P.a_new, acc[k][4], knew[k][4]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NQ; ++k)
+#pragma unroll
+      for (int v = 0; v < 5; ++v) oe[v * N3 + k * N2] = knew[k][v];
+    if (update) {
+      // LSRK register update folded into the same pass (Solver::axpy,
+      // solver.hpp:342-353): q_next = q + b k. q is double buffered
+      // because neighbouring CTAs still read this element's faces.
+      Real* __restrict__ qn = P.q_next + eg * (5 * N3) + l;
+#pragma unroll
+      for (int k = 0; k < NQ; ++k)
+#pragma unroll
+        for (int v = 0; v < 5; ++v)
+          qn[v * N3 + k * N2] = qv[k][v] + P.b_upd * knew[k][v];
     }
   }
 }
