@@ -13,7 +13,8 @@ cudaError_t launch_one(const dev::RhsParams<Real, NQ>& P, cudaStream_t stream) {
   constexpr int MINB = dev::Tile<NQ, sizeof(Real)>::MINB;
   constexpr int T = EPB * NQ * NQ;
   constexpr size_t smem =
-      size_t(dev::V_COUNT + 5) * EPB * dev::Geo<NQ>::N3P * sizeof(Real);
+      (size_t(dev::V_COUNT + 5) * EPB * dev::Geo<NQ>::N3P + dev::LogTab<Real>::kReals) *
+      sizeof(Real);
   auto kern = dev::rhs_kernel<Real, NQ, EPB, MINB, VOL, SURF>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -58,7 +59,8 @@ void rhs_launch_shape(int* threads, int* epb, size_t* smem_bytes) {
   constexpr int EPB = dev::Tile<NQ, sizeof(Real)>::EPB;
   *threads = EPB * NQ * NQ;
   *epb = EPB;
-  *smem_bytes = size_t(dev::V_COUNT + 5) * EPB * dev::Geo<NQ>::N3P * sizeof(Real);
+  *smem_bytes = (size_t(dev::V_COUNT + 5) * EPB * dev::Geo<NQ>::N3P +
+                 dev::LogTab<Real>::kReals) * sizeof(Real);
 }
 
 #define ESDG_INSTANTIATE(REAL, NQ)                                             \

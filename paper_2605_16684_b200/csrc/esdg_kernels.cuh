@@ -223,7 +223,7 @@ __device__ __forceinline__ void face_contribution(const RhsParams<Real, NQ>& P,
                                                   const Node<Real>& own,
                                                   const NbrRaw<Real>& nbr, int dir,
                                                   int side, long long eg, int fn,
-                                                  Real c[5]) {
+                                                  const Real* logtab, Real c[5]) {
   Node<Real> nb;
   if (nbr.code == -1) {
     // reflecting wall: mirror state, phi+ = phi- (kernels.hpp:364-367)
@@ -231,7 +231,7 @@ __device__ __forceinline__ void face_contribution(const RhsParams<Real, NQ>& P,
     nb.hun = -own.hun;
   } else {
     Real nv[V_COUNT], pr;
-    if (!node_vals(nbr.q, nbr.ph, P.gas.gm1, nv, pr))
+    if (!node_vals(nbr.q, nbr.ph, P.gas.gm1, logtab, nv, pr))
       raise_flag(P.flag, P.flag_records, P.stage, 1, P.elem_offset + eg, fn,
                  double(nbr.q[0]), double(pr));
     nb = rotate_node(nv, dir);
@@ -267,19 +267,18 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Real* vals = reinterpret_cast<Real*>(smem_raw); // [V_COUNT][VS]
   Real* tend = vals + V_COUNT * VS;               // [5][VS]
+  Real* logtab = tend + 5 * VS;                   // FP64 only: logarithm table
 
   const int tid = threadIdx.x;
   const long long e0 = static_cast<long long>(blockIdx.x) * EPB;
-  const long long left = P.ne - e0;
-  const int ne_blk = left < EPB ? static_cast<int>(left) : EPB;
 
   // thread <-> (element e, line l = l0 + NQ l1). In phase A, in the z sweep
   // and in the commit the thread owns the z line through (x, y) = (l0, l1),
   // so those three stages hand data over in registers.
   const int e = tid / N2, l = tid - e * N2;
-  const bool active = e < ne_blk;
   const int l0 = l % NQ, l1 = l / NQ;
   const long long eg = e0 + e;
+  const bool active = eg < P.ne; // only the last CTA has idle lines
   const int zbase = e * N3P + l0 + PX * l1;
   const bool read_out = !VOL || P.a_old != Real(0);
 
@@ -326,10 +325,12 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // every later phase adds a_new * (its contribution); the commit then has
   // no global load left to wait for.
   const Real a_keep = VOL ? P.a_old : Real(1);
+  const Real* qe = P.q + eg * (5 * N3) + l;
+  const Real* pe = P.phi + eg * N3 + l;
+  Real qv[NQ][5], ph[NQ], ltab[kLogTabRegs];
+  static_assert(EPB * N2 * kLogTabRegs >= LogTab<Real>::kReals, "CTA too small for the table");
+  load_log_table(ltab, tid, EPB * N2);
   if (active) {
-    const Real* qe = P.q + eg * (5 * N3) + l;
-    const Real* pe = P.phi + eg * N3 + l;
-    Real qv[NQ][5], ph[NQ];
 #pragma unroll
     for (int k = 0; k < NQ; ++k) {
 #pragma unroll
@@ -373,26 +374,31 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         }
       }
     }
+  }
+  // the logarithm's table (FP64): fetched behind the state loads, visible to
+  // the CTA before the first logarithm
+  store_log_table(logtab, ltab, tid, EPB * N2);
+  if (sizeof(Real) == 8) __syncthreads();
+  if (active) {
     if (SURF) fetch(0, cur); // first face's neighbour trace: lands during the logs
-    // The NQ nodes are independent: no branch separates them, so their
+    // The NQ nodes are independent and computed stage by stage so that their
     // reciprocal and logarithm chains interleave. A non-physical node is
     // only remembered here and reported after the loop.
-    int bad = -1;
+    Real nvs[NQ][V_COUNT], prs[NQ];
+    const unsigned badmask = node_vals_line<Real, NQ>(qv, ph, P.gas.gm1, logtab, nvs, prs);
 #pragma unroll
     for (int k = 0; k < NQ; ++k) {
-      Real nv[V_COUNT], pr;
-      const bool ok = node_vals(qv[k], ph[k], P.gas.gm1, nv, pr);
-      bad = (!ok && bad < 0) ? k : bad;
       const int s = zbase + k * ZS;
 #pragma unroll
-      for (int j = 0; j < V_COUNT; ++j) vals[j * VS + s] = nv[j];
+      for (int j = 0; j < V_COUNT; ++j) vals[j * VS + s] = nvs[k][j];
     }
+    const int bad = badmask ? __ffs(badmask) - 1 : -1;
     if (bad >= 0) {
       const Real* qb = qe + bad * N2;
       Real qq[5], nv[V_COUNT], pr;
 #pragma unroll
       for (int v = 0; v < 5; ++v) qq[v] = qb[v * N3];
-      node_vals(qq, pe[bad * N2], P.gas.gm1, nv, pr);
+      node_vals(qq, pe[bad * N2], P.gas.gm1, logtab, nv, pr);
       raise_flag(P.flag, P.flag_records, P.stage, 0, P.elem_offset + eg, l + bad * N2,
                  double(qq[0]), double(pr));
     }
@@ -416,7 +422,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
                           l0 * spitch(d1) + l1 * spitch(d2);
         const Node<Real> own = load_node(vals, VS, s_own, dir);
         Real c[5];
-        face_contribution<Real, NQ>(P, own, cur, dir, side, eg, l, c);
+        face_contribution<Real, NQ>(P, own, cur, dir, side, eg, l, logtab, c);
         const Real o0 = tend[s_own], o1 = tend[(1 + dir) * VS + s_own],
                    o2 = tend[(1 + d1) * VS + s_own], o3 = tend[(1 + d2) * VS + s_own],
                    o4 = tend[4 * VS + s_own];
@@ -440,7 +446,11 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
 #pragma unroll
     for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
   if (VOL) {
+#ifdef ESDG_TUNE_UNROLL_DIR
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
     for (int dir = 0; dir < 3; ++dir) {
       if (active) {
         const int base = dir == 0 ? e * N3P + PX * l
@@ -632,7 +642,11 @@ struct Tile;
 template <> struct Tile<2, 8> { static constexpr int EPB = 32, MINB = 4; };
 template <> struct Tile<3, 8> { static constexpr int EPB = 14, MINB = 4; };
 template <> struct Tile<4, 8> { static constexpr int EPB = 8, MINB = 3; };
-template <> struct Tile<5, 8> { static constexpr int EPB = 5, MINB = 3; };
+#ifndef ESDG_TUNE_EPB
+#define ESDG_TUNE_EPB 5
+#define ESDG_TUNE_MINB 3
+#endif
+template <> struct Tile<5, 8> { static constexpr int EPB = ESDG_TUNE_EPB, MINB = ESDG_TUNE_MINB; };
 template <> struct Tile<6, 8> { static constexpr int EPB = 3, MINB = 2; };
 template <> struct Tile<7, 8> { static constexpr int EPB = 2, MINB = 2; };
 template <> struct Tile<8, 8> { static constexpr int EPB = 2, MINB = 1; };

@@ -24,7 +24,7 @@ SRC = textwrap.dedent(r"""
           case 2: x = 1.16 * (1 + 0.1 * (u - 0.5)); break;   // densities
           default: x = 5.8e-6 * (1 + 0.2 * (u - 0.5));       // rho / (2 p)
         }
-        const double got = esdg_b200::dev::log_pos(x);
+        const double got = esdg_b200::dev::log_pos(x, esdg_b200::dev::h_log_table);
         const long double ref = logl((long double)x);
         const double rr = (double)ref;
         const double ulp = std::fabs(std::nextafter(rr, INFINITY) - rr);
