@@ -12,9 +12,12 @@ cudaError_t launch_one(const dev::RhsParams<Real, NQ>& P, cudaStream_t stream) {
   constexpr int EPB = dev::Tile<NQ, sizeof(Real)>::EPB;
   constexpr int MINB = dev::Tile<NQ, sizeof(Real)>::MINB;
   constexpr int T = EPB * NQ * NQ;
+#ifndef ESDG_TUNE_EXTRA_SMEM
+#define ESDG_TUNE_EXTRA_SMEM 0
+#endif
   constexpr size_t smem =
       (size_t(dev::V_COUNT + 5) * EPB * dev::Geo<NQ>::N3P + dev::LogTab<Real>::kReals) *
-      sizeof(Real);
+          sizeof(Real) + ESDG_TUNE_EXTRA_SMEM;
   auto kern = dev::rhs_kernel<Real, NQ, EPB, MINB, VOL, SURF>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;

@@ -56,6 +56,7 @@ struct RhsParams {
   long long ne;
   long long elem_offset;
   Real a_old, a_new, b_upd;
+  Real gain, fin; // slab arithmetic, see rhs_kernel phase A (set by the host)
   GasParams<Real> gas;
   Real negc[3][NQ * NQ]; // -(2 g_d D_ij), kernels.hpp:187, 224-225
   Real lift[3];          // Operators::face_coef, kernels.hpp:86-88
@@ -97,6 +98,18 @@ __device__ __forceinline__ void raise_flag(unsigned long long* flag,
     __threadfence();
     r->key = key;
   }
+}
+
+// Asynchronous global -> shared copy of one Real (LDGSTS): no register
+// staging, and the issuing thread does not wait for the data.
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem_dst, const void* gmem_src) {
+  const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst), "l"(gmem_src), "n"(BYTES)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 template <int NQ>
@@ -319,12 +332,13 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   };
 
   // ---- phase A: primitives and logarithms, once per node ------------------
-  // All global loads -- the state, the geopotential and (accumulate form) the
-  // old contents of `out` -- are issued before the first logarithm, so the
-  // CTA pays for one HBM round trip. The slab starts as a_old * out_old and
-  // every later phase adds a_new * (its contribution); the commit then has
-  // no global load left to wait for.
-  const Real a_keep = VOL ? P.a_old : Real(1);
+  // All global loads are issued before the first logarithm, so the CTA pays
+  // for one HBM round trip. In the accumulate form the old contents of `out`
+  // go straight into the slab (asynchronous copies, nobody waits for them
+  // before the barrier that ends phase A). The slab then holds
+  //   T = out_old + gain * (contributions),  gain = a_new / a_old,
+  // and the commit writes out = a_old * T; with a_old == 0 it holds
+  // a_new * (contributions) and `out` is never read.
   const Real* qe = P.q + eg * (5 * N3) + l;
   const Real* pe = P.phi + eg * N3 + l;
   Real qv[NQ][5], ph[NQ], ltab[kLogTabRegs];
@@ -339,16 +353,11 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     }
     if (read_out) {
       const Real* oe = P.out + eg * (5 * N3) + l;
-      Real ov[NQ][5];
-#pragma unroll
-      for (int k = 0; k < NQ; ++k)
-#pragma unroll
-        for (int v = 0; v < 5; ++v) ov[k][v] = oe[v * N3 + k * N2];
 #pragma unroll
       for (int k = 0; k < NQ; ++k)
 #pragma unroll
         for (int v = 0; v < 5; ++v)
-          tend[v * VS + zbase + k * ZS] = VOL ? a_keep * ov[k][v] : ov[k][v];
+          cp_async<sizeof(Real)>(&tend[v * VS + zbase + k * ZS], oe + v * N3 + k * N2);
     } else if (SURF) {
       // the faces are the slab's first writers and touch surface nodes only
 #pragma unroll
@@ -403,6 +412,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
                  double(qq[0]), double(pr));
     }
   }
+  cp_async_wait_all(); // this thread's share of out_old is in the slab
   __syncthreads();
 
   // ---- phase C: the six faces, thread per face node -----------------------
@@ -426,11 +436,11 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         const Real o0 = tend[s_own], o1 = tend[(1 + dir) * VS + s_own],
                    o2 = tend[(1 + d1) * VS + s_own], o3 = tend[(1 + d2) * VS + s_own],
                    o4 = tend[4 * VS + s_own];
-        tend[s_own] = fma_(-P.a_new, c[0], o0);
-        tend[(1 + dir) * VS + s_own] = fma_(-P.a_new, c[1], o1);
-        tend[(1 + d1) * VS + s_own] = fma_(-P.a_new, c[2], o2);
-        tend[(1 + d2) * VS + s_own] = fma_(-P.a_new, c[3], o3);
-        tend[4 * VS + s_own] = fma_(-P.a_new, c[4], o4);
+        tend[s_own] = fma_(-P.gain, c[0], o0);
+        tend[(1 + dir) * VS + s_own] = fma_(-P.gain, c[1], o1);
+        tend[(1 + d1) * VS + s_own] = fma_(-P.gain, c[2], o2);
+        tend[(1 + d2) * VS + s_own] = fma_(-P.gain, c[3], o3);
+        tend[4 * VS + s_own] = fma_(-P.gain, c[4], o4);
         cur = nxt;
       }
       if (lf & 1) __syncthreads();
@@ -486,12 +496,12 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
 #pragma unroll
             for (int i = 0; i < NQ; ++i)
 #pragma unroll
-              for (int v = 0; v < 5; ++v) acc[i][v] = fma_(P.a_new, acc[i][v], old[i][v]);
+              for (int v = 0; v < 5; ++v) acc[i][v] = fma_(P.gain, acc[i][v], old[i][v]);
           } else {
 #pragma unroll
             for (int i = 0; i < NQ; ++i)
 #pragma unroll
-              for (int v = 0; v < 5; ++v) acc[i][v] = P.a_new * acc[i][v];
+              for (int v = 0; v < 5; ++v) acc[i][v] = P.gain * acc[i][v];
           }
 #pragma unroll
           for (int i = 0; i < NQ; ++i) {
@@ -552,11 +562,11 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
       }
 #pragma unroll
       for (int k = 0; k < NQ; ++k) {
-        knew[k][0] = fma_(P.a_new, acc[k][0], knew[k][0]);
-        knew[k][1] = fma_(P.a_new, acc[k][2], knew[k][1]);
-        knew[k][2] = fma_(P.a_new, acc[k][3], knew[k][2]);
-        knew[k][3] = fma_(P.a_new, acc[k][1], knew[k][3]);
-        knew[k][4] = fma_(P.a_new, acc[k][4], knew[k][4]);
+        knew[k][0] = P.fin * fma_(P.gain, acc[k][0], knew[k][0]);
+        knew[k][1] = P.fin * fma_(P.gain, acc[k][2], knew[k][1]);
+        knew[k][2] = P.fin * fma_(P.gain, acc[k][3], knew[k][2]);
+        knew[k][3] = P.fin * fma_(P.gain, acc[k][1], knew[k][3]);
+        knew[k][4] = P.fin * fma_(P.gain, acc[k][4], knew[k][4]);
       }
     }
 #pragma unroll

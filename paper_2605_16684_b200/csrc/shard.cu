@@ -313,6 +313,9 @@ private:
     P.elem_offset = elem_offset_;
     P.a_old = Real(a_old);
     P.a_new = Real(a_new);
+    // slab arithmetic of rhs_kernel: T = out_old + gain * rhs, out = fin * T
+    P.gain = P.a_old != Real(0) ? P.a_new / P.a_old : P.a_new;
+    P.fin = P.a_old != Real(0) ? P.a_old : Real(1);
     P.gas = gas_;
     for (int k = 0; k < 3; ++k) {
       for (int i = 0; i < NQ * NQ; ++i)
