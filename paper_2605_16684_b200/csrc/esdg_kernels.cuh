@@ -58,7 +58,8 @@ struct RhsParams {
   Real a_old, a_new, b_upd;
   Real gain, fin; // slab arithmetic, see rhs_kernel phase A (set by the host)
   GasParams<Real> gas;
-  Real negc[3][NQ * NQ]; // -(2 g_d D_ij), kernels.hpp:187, 224-225
+  Real negd[NQ * NQ];    // -(2 D_ij); with metric[d]: -(2 g_d D_ij), kernels.hpp:187, 224-225
+  Real metric[3];        // g_d = 2 / dx_d
   Real lift[3];          // Operators::face_coef, kernels.hpp:86-88
   int prefetch_ctas;     // resident CTAs chip-wide: L2 prefetch distance
   int with_source;       // Coriolis on (commit_volume, solver.hpp:205-216)
@@ -163,7 +164,11 @@ __device__ __forceinline__ Node<Real> rotate_node(const Real nv[V_COUNT],
 // One line sweep of the flux-differenced volume term in direction `dir`
 // (sweep_direction, kernels.hpp:154-249): pulls the NQ nodes of a line into
 // registers, ADDS the diagonal point fluxes and every unordered pair (once)
-// to acc, which lives in the rotated frame of `dir`. One code instance
+// to acc, which lives in the rotated frame of `dir` and still lacks the
+// metric factor g_dir: the coefficients -(2 D_ij) are then the same in every
+// direction and enter the FMAs as immediate constant-bank operands (an FP64
+// instruction reading three distinct vector registers occupies the sm_100
+// FP64 pipe for three cycles instead of two). One code instance
 // serves the three directions (the instruction cache is a real constraint
 // for these fully unrolled bodies).
 template <class Real, int NQ>
@@ -179,7 +184,7 @@ __device__ __forceinline__ void sweep_line(const RhsParams<Real, NQ>& P,
   // carry a point flux -- known at compile time, no branch.
 #pragma unroll
   for (int i = 0; i < NQ; i += NQ - 1) {
-    const Real cii = P.negc[dir][i * NQ + i];
+    const Real cii = P.negd[i * NQ + i];
     Real f[5];
     point_flux(nd[i], P.gas.cg, f);
 #pragma unroll
@@ -192,8 +197,8 @@ __device__ __forceinline__ void sweep_line(const RhsParams<Real, NQ>& P,
     for (int j = 0; j < NQ; ++j) {
       if (j <= i) continue; // constant bounds keep the unroll total
       const PairFlux<Real> pf = pair_flux(nd[i], nd[j], P.gas.cg);
-      const Real cij = P.negc[dir][i * NQ + j];
-      const Real cji = P.negc[dir][j * NQ + i];
+      const Real cij = P.negd[i * NQ + j];
+      const Real cji = P.negd[j * NQ + i];
       const Real fni = fma_(pf.tg, nd[i].hib, pf.f[1]);
       const Real fnj = fma_(-pf.tg, nd[j].hib, pf.f[1]);
       acc[i][0] = fma_(cij, pf.f[0], acc[i][0]);
@@ -269,6 +274,71 @@ __device__ __forceinline__ void face_contribution(const RhsParams<Real, NQ>& P,
   for (int v = 0; v < 5; ++v) c[v] = lift * (fl[v] - n_own * fo[v]);
 }
 
+// The two faces of one direction (side 0 at node 0, side 1 at node NQ-1 of
+// the line through the face node) share no data, so their evaluations are
+// written stage by stage: two independent dependency chains for the
+// scheduler instead of one. Same arithmetic as face_contribution per face.
+template <class Real, int NQ>
+__device__ __forceinline__ void face_pair_contribution(const RhsParams<Real, NQ>& P,
+                                                       const Node<Real> (&own)[2],
+                                                       const NbrRaw<Real> (&nbr)[2], int dir,
+                                                       long long eg, int fn,
+                                                       const Real* logtab, Real (&c)[2][5]) {
+  Real q2[2][5], ph2[2], nv[2][V_COUNT], pr[2];
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+#pragma unroll
+    for (int v = 0; v < 5; ++v) q2[f][v] = nbr[f].q[v];
+    ph2[f] = nbr[f].ph;
+  }
+  const unsigned bad = node_vals_line<Real, 2>(q2, ph2, P.gas.gm1, logtab, nv, pr);
+  Node<Real> nb[2];
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    nb[f] = rotate_node(nv[f], dir);
+    if (nbr[f].code == -1) {
+      // reflecting wall: mirror state, phi+ = phi- (kernels.hpp:364-367); the
+      // values computed from the placeholder trace are discarded
+      nb[f] = own[f];
+      nb[f].hun = -own[f].hun;
+    } else if (bad & (1u << f)) {
+      raise_flag(P.flag, P.flag_records, P.stage, 1, P.elem_offset + eg, fn,
+                 double(q2[f][0]), double(pr[f]));
+    }
+  }
+  PairFlux<Real> pf[2];
+#pragma unroll
+  for (int f = 0; f < 2; ++f) pf[f] = pair_flux(own[f], nb[f], P.gas.cg);
+  Real dd[2][5];
+#pragma unroll
+  for (int f = 0; f < 2; ++f)
+#pragma unroll
+    for (int v = 0; v < 5; ++v) dd[f][v] = Real(0);
+  if (P.dissipation) {
+#pragma unroll
+    for (int f = 0; f < 2; ++f)
+      matrix_dissipation(own[f], nb[f], pf[f].rho_log, pf[f].inv_blog, P.gas, dd[f]);
+  }
+  const Real lift = P.lift[dir];
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    Real fo[5];
+    point_flux(own[f], P.gas.cg, fo);
+    // commit_face_side (kernels.hpp:391-430)
+    const Real n_own = f ? Real(1) : Real(-1);
+    const Real g_own = pf[f].tg * own[f].hib;
+    const Real phi_own = own[f].hphi + own[f].hphi;
+    Real fl[5];
+    fl[0] = n_own * pf[f].f[0] - Real(0.5) * dd[f][0];
+    fl[1] = n_own * pf[f].f[1] + n_own * g_own - Real(0.5) * dd[f][1];
+    fl[2] = n_own * pf[f].f[2] - Real(0.5) * dd[f][2];
+    fl[3] = n_own * pf[f].f[3] - Real(0.5) * dd[f][3];
+    fl[4] = n_own * pf[f].f[4] - Real(0.5) * fma_(phi_own, dd[f][0], dd[f][4]);
+#pragma unroll
+    for (int v = 0; v < 5; ++v) c[f][v] = lift * (fl[v] - n_own * fo[v]);
+  }
+}
+
 template <class Real, int NQ, int EPB, int MINB, bool VOL, bool SURF>
 __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     rhs_kernel(const __grid_constant__ RhsParams<Real, NQ> P) {
@@ -308,7 +378,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // Neighbour state of face lf, fetched one face ahead of its use so the
   // (mostly L2-resident) gather hides behind arithmetic. The six neighbour
   // codes were read at kernel start, so a fetch is one round trip, not two.
-  NbrRaw<Real> cur, nxt;
+  NbrRaw<Real> cur[2], nxt[2];
   auto fetch = [&](int lf, NbrRaw<Real>& r) {
     const int dir = lf >> 1, side = lf & 1;
     const int d1 = dir == 2 ? 0 : dir + 1;
@@ -328,6 +398,11 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
 #pragma unroll
       for (int v = 0; v < 5; ++v) r.q[v] = P.ghost_q[(g * 5 + v) * N2 + l];
       r.ph = P.ghost_phi[g * N2 + l];
+    } else {
+      // reflecting wall: no trace; a harmless placeholder state
+#pragma unroll
+      for (int v = 0; v < 5; ++v) r.q[v] = Real(v == 0 || v == 4);
+      r.ph = Real(0);
     }
   };
 
@@ -389,7 +464,10 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   store_log_table(logtab, ltab, tid, EPB * N2);
   if (sizeof(Real) == 8) __syncthreads();
   if (active) {
-    if (SURF) fetch(0, cur); // first face's neighbour trace: lands during the logs
+    if (SURF) { // the first direction's neighbour traces: they land during the logs
+      fetch(0, cur[0]);
+      fetch(1, cur[1]);
+    }
     // The NQ nodes are independent and computed stage by stage so that their
     // reciprocal and logarithm chains interleave. A non-physical node is
     // only remembered here and reported after the loop.
@@ -421,29 +499,46 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // faces of different directions do (edges), hence the two barriers.
   if (SURF) {
 #pragma unroll 1
-    for (int lf = 0; lf < 6; ++lf) {
+    for (int dir = 0; dir < 3; ++dir) {
       if (active) {
-        if (lf < 5) fetch(lf + 1, nxt);
-        const int dir = lf >> 1, side = lf & 1;
+        if (dir < 2) {
+          fetch(2 * dir + 2, nxt[0]);
+          fetch(2 * dir + 3, nxt[1]);
+        }
         const int d1 = dir == 2 ? 0 : dir + 1;
         const int d2 = d1 == 2 ? 0 : d1 + 1;
         // FaceIndexer::node (mesh.hpp:107-114): tangential axes d1, d2
-        const int s_own = e * N3P + (side ? NQ - 1 : 0) * spitch(dir) +
-                          l0 * spitch(d1) + l1 * spitch(d2);
-        const Node<Real> own = load_node(vals, VS, s_own, dir);
-        Real c[5];
-        face_contribution<Real, NQ>(P, own, cur, dir, side, eg, l, logtab, c);
-        const Real o0 = tend[s_own], o1 = tend[(1 + dir) * VS + s_own],
-                   o2 = tend[(1 + d1) * VS + s_own], o3 = tend[(1 + d2) * VS + s_own],
-                   o4 = tend[4 * VS + s_own];
-        tend[s_own] = fma_(-P.gain, c[0], o0);
-        tend[(1 + dir) * VS + s_own] = fma_(-P.gain, c[1], o1);
-        tend[(1 + d1) * VS + s_own] = fma_(-P.gain, c[2], o2);
-        tend[(1 + d2) * VS + s_own] = fma_(-P.gain, c[3], o3);
-        tend[4 * VS + s_own] = fma_(-P.gain, c[4], o4);
-        cur = nxt;
+        const int s0 = e * N3P + l0 * spitch(d1) + l1 * spitch(d2);
+        const int s_own[2] = {s0, s0 + (NQ - 1) * spitch(dir)};
+        Node<Real> own[2];
+        own[0] = load_node(vals, VS, s_own[0], dir);
+        own[1] = load_node(vals, VS, s_own[1], dir);
+        Real c[2][5], o[2][5];
+        face_pair_contribution<Real, NQ>(P, own, cur, dir, eg, l, logtab, c);
+        Real* tn = tend + (1 + dir) * VS;
+        Real* tt1 = tend + (1 + d1) * VS;
+        Real* tt2 = tend + (1 + d2) * VS;
+        Real* t4 = tend + 4 * VS;
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+          o[f][0] = tend[s_own[f]];
+          o[f][1] = tn[s_own[f]];
+          o[f][2] = tt1[s_own[f]];
+          o[f][3] = tt2[s_own[f]];
+          o[f][4] = t4[s_own[f]];
+        }
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+          tend[s_own[f]] = fma_(-P.gain, c[f][0], o[f][0]);
+          tn[s_own[f]] = fma_(-P.gain, c[f][1], o[f][1]);
+          tt1[s_own[f]] = fma_(-P.gain, c[f][2], o[f][2]);
+          tt2[s_own[f]] = fma_(-P.gain, c[f][3], o[f][3]);
+          t4[s_own[f]] = fma_(-P.gain, c[f][4], o[f][4]);
+        }
+        cur[0] = nxt[0];
+        cur[1] = nxt[1];
       }
-      if (lf & 1) __syncthreads();
+      __syncthreads();
     }
   }
 
@@ -482,6 +577,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           Real* tt1 = tend + (1 + d1) * VS;
           Real* tt2 = tend + (1 + d2) * VS;
           Real* t4 = tend + 4 * VS;
+          const Real scale = P.gain * P.metric[dir];
           if (SURF || dir != 0 || read_out) {
             Real old[NQ][5];
 #pragma unroll
@@ -496,12 +592,12 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
 #pragma unroll
             for (int i = 0; i < NQ; ++i)
 #pragma unroll
-              for (int v = 0; v < 5; ++v) acc[i][v] = fma_(P.gain, acc[i][v], old[i][v]);
+              for (int v = 0; v < 5; ++v) acc[i][v] = fma_(scale, acc[i][v], old[i][v]);
           } else {
 #pragma unroll
             for (int i = 0; i < NQ; ++i)
 #pragma unroll
-              for (int v = 0; v < 5; ++v) acc[i][v] = P.gain * acc[i][v];
+              for (int v = 0; v < 5; ++v) acc[i][v] = scale * acc[i][v];
           }
 #pragma unroll
           for (int i = 0; i < NQ; ++i) {
@@ -552,22 +648,29 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
       for (int v = 0; v < 5; ++v) knew[k][v] = tend[v * VS + s];
     }
     if (VOL) {
+      // acc still lacks the z metric
+      const Real zscale = P.gain * P.metric[2];
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) {
+        knew[k][0] = fma_(zscale, acc[k][0], knew[k][0]);
+        knew[k][1] = fma_(zscale, acc[k][2], knew[k][1]);
+        knew[k][2] = fma_(zscale, acc[k][3], knew[k][2]);
+        knew[k][3] = fma_(zscale, acc[k][1], knew[k][3]);
+        knew[k][4] = fma_(zscale, acc[k][4], knew[k][4]);
+      }
       if (source) {
         // h = (0, f q2, -f q1, 0, 0)
+        const Real gcf = P.gain * cf;
 #pragma unroll
         for (int k = 0; k < NQ; ++k) {
-          acc[k][2] = acc[k][2] + cf * qv[k][2];
-          acc[k][3] = acc[k][3] + (-cf) * qv[k][1];
+          knew[k][1] = fma_(gcf, qv[k][2], knew[k][1]);
+          knew[k][2] = fma_(-gcf, qv[k][1], knew[k][2]);
         }
       }
 #pragma unroll
-      for (int k = 0; k < NQ; ++k) {
-        knew[k][0] = P.fin * fma_(P.gain, acc[k][0], knew[k][0]);
-        knew[k][1] = P.fin * fma_(P.gain, acc[k][2], knew[k][1]);
-        knew[k][2] = P.fin * fma_(P.gain, acc[k][3], knew[k][2]);
-        knew[k][3] = P.fin * fma_(P.gain, acc[k][1], knew[k][3]);
-        knew[k][4] = P.fin * fma_(P.gain, acc[k][4], knew[k][4]);
-      }
+      for (int k = 0; k < NQ; ++k)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) knew[k][v] = P.fin * knew[k][v];
     }
 #pragma unroll
     for (int k = 0; k < NQ; ++k)

@@ -73,10 +73,13 @@ public:
       metric_[k] = Real(d.metric[k]);
       lift_[k] = metric_[k] / w[0];
     }
-    negc_.assign(size_t(3 * n2_), Real(0));
-    for (int k = 0; k < 3; ++k)
-      for (int i = 0; i < n2_; ++i)
-        negc_[size_t(k * n2_ + i)] = -(Real(2) * metric_[k] * D[size_t(i)]);
+    // The flux-differencing coefficient -(2 g_d D_ij) (kernels.hpp:187,
+    // 224-225) is applied in two factors: -(2 D_ij) inside the line sweep --
+    // the same for all three directions, so the kernel reads it as an
+    // immediate constant-bank operand -- and the metric g_d once per node
+    // when the sweep's sums are handed on.
+    negd_.assign(size_t(n2_), Real(0));
+    for (int i = 0; i < n2_; ++i) negd_[size_t(i)] = -(Real(2) * D[size_t(i)]);
     // D_ii is analytically zero at interior LGL nodes; the negative-row-sum
     // construction (reference_element.cpp:135) leaves an O(1e-16) residue.
     // Flush it so the kernel can skip those point fluxes: the dropped term is
@@ -84,7 +87,7 @@ public:
     for (int i = 1; i + 1 < nq_; ++i) {
       const double dii = std::abs(d.diff[i * nq_ + i]);
       if (dii <= 1e-13 * std::abs(d.diff[0]))
-        for (int k = 0; k < 3; ++k) negc_[size_t(k * n2_ + i * nq_ + i)] = Real(0);
+        negd_[size_t(i * nq_ + i)] = Real(0);
     }
     const Real gamma = Real(d.gamma), R = Real(d.gas_R);
     gas_.gamma = gamma;
@@ -317,9 +320,9 @@ private:
     P.gain = P.a_old != Real(0) ? P.a_new / P.a_old : P.a_new;
     P.fin = P.a_old != Real(0) ? P.a_old : Real(1);
     P.gas = gas_;
+    for (int i = 0; i < NQ * NQ; ++i) P.negd[i] = negd_[size_t(i)];
     for (int k = 0; k < 3; ++k) {
-      for (int i = 0; i < NQ * NQ; ++i)
-        P.negc[k][i] = negc_[size_t(k * NQ * NQ + i)];
+      P.metric[k] = metric_[k];
       P.lift[k] = lift_[k];
     }
     P.with_source = (with_source && coriolis_mode_ != 0) ? 1 : 0;
@@ -382,7 +385,7 @@ private:
   int64_t ne_ = 0, elem_offset_ = 0, n_ghost_ = 0, n_send_ = 0;
   int dissipation_ = 1, coriolis_mode_ = 0;
   Real metric_[3] = {0, 0, 0}, lift_[3] = {0, 0, 0};
-  std::vector<Real> negc_;
+  std::vector<Real> negd_;
   dev::GasParams<Real> gas_{};
   Real *q_ = nullptr, *q_alt_ = nullptr, *k_ = nullptr, *phi_ = nullptr, *ghost_phi_ = nullptr;
   Real *recv_ = nullptr, *send_ = nullptr, *cor_f_ = nullptr;
