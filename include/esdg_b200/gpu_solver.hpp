@@ -282,6 +282,14 @@ public:
            weights_[size_t(c)];
   }
 
+  // Where the diagnostics and compute_dt are reduced: on the device (default;
+  // one double per element crosses PCIe) or on the host in the reference's
+  // summation order (bitwise the reference's sums, moves the state).
+  void set_reduction_on_host(bool on) {
+    guard(esdg_b200_solver_set_reduction(
+              solver_, on ? ESDG_B200_REDUCE_ON_HOST : ESDG_B200_REDUCE_ON_DEVICE), -1);
+  }
+
   // diagnostics of the internal registers (diagnostics.hpp:30-106)
   double quadrature_total(int var) {
     restore_internal();

@@ -297,6 +297,10 @@ int esdg_b200_solver_entropy_production(esdg_b200_solver* s, double* out) {
   CORE(s);
   return out ? c.entropy_production(out) : ESDG_B200_BADARG;
 }
+int esdg_b200_solver_set_reduction(esdg_b200_solver* s, int mode) {
+  CORE(s);
+  return c.set_reduction(mode);
+}
 int esdg_b200_solver_enable_timing(esdg_b200_solver* s, int on) {
   CORE(s);
   return c.enable_timing(on != 0);

@@ -651,7 +651,7 @@ struct Neumaier {
 
 // compute_stable_dt (time_integration.hpp:55-92), 64-bit, on the downloaded
 // state; startup-only in the reference's runner (runner.cpp:150-153)
-int SolverCore::compute_dt(double courant, double* dt_out) {
+int SolverCore::compute_dt_host(double courant, double* dt_out) {
   std::vector<double> gap(static_cast<size_t>(nq_));
   for (int i = 0; i < nq_; ++i) {
     double g = 2.0;
@@ -703,7 +703,7 @@ int SolverCore::compute_dt(double courant, double* dt_out) {
 
 // quadrature_total (diagnostics.hpp:30-47): serial Neumaier sum in element /
 // node order, identical to the reference's summation order
-int SolverCore::quadrature_total(int reg, int var, double* out) {
+int SolverCore::quadrature_total_host(int reg, int var, double* out) {
   if (var < 0 || var > 4 || (reg != 0 && reg != 1)) return ESDG_B200_BADARG;
   const double J = mesh_->jacobian;
   const int prec = opt_.precision;
@@ -721,7 +721,7 @@ int SolverCore::quadrature_total(int reg, int var, double* out) {
 }
 
 // total_entropy (diagnostics.hpp:49-71)
-int SolverCore::total_entropy(double* out) {
+int SolverCore::total_entropy_host(double* out) {
   const double J = mesh_->jacobian, gamma = opt_.gas.gamma, grav = opt_.gas.gravity;
   const int prec = opt_.precision;
   Neumaier sum;
@@ -754,7 +754,7 @@ int SolverCore::total_entropy(double* out) {
 
 // entropy_production (diagnostics.hpp:73-106) of the pair (q register,
 // k register): sum J w^3 v(q) . k
-int SolverCore::entropy_production(double* out) {
+int SolverCore::entropy_production_host(double* out) {
   const double J = mesh_->jacobian, gamma = opt_.gas.gamma, grav = opt_.gas.gravity;
   const int prec = opt_.precision;
   Neumaier sum;
@@ -790,6 +790,106 @@ int SolverCore::entropy_production(double* out) {
     for (double v : term) sum.add(v);
   }));
   if (bad) return ESDG_B200_NONPHYSICAL;
+  *out = sum.value();
+  return ESDG_B200_OK;
+}
+
+// ---- device-evaluated reductions (K6) -----------------
+// The per-node terms are evaluated on the GPU in 64-bit exactly as the host
+// versions above write them and summed per element with Neumaier
+// compensation; only one double per element crosses PCIe (7 MB instead of
+// 4.4 GB at configs[1]). The host finishes with a compensated sum in Morton
+// order. compute_dt is a minimum and therefore bitwise the host value; the
+// sums agree with the reference's single serial chain to rounding of the
+// result (the tests state 1e-14 relative). ESDG_B200_REDUCE_ON_HOST selects
+// the host versions, which reproduce the reference's summation order
+// bitwise.
+
+int SolverCore::set_reduction(int mode) {
+  if (mode != ESDG_B200_REDUCE_ON_DEVICE && mode != ESDG_B200_REDUCE_ON_HOST)
+    return ESDG_B200_BADARG;
+  reduction_ = mode;
+  return ESDG_B200_OK;
+}
+
+int SolverCore::device_partials(int kind, int reg, int var, std::vector<double>& partials,
+                                bool& bad) {
+  std::vector<double> weight(static_cast<size_t>(n3_)), dx(static_cast<size_t>(3 * nq_));
+  const double J = mesh_->jacobian;
+  for (int n = 0; n < n3_; ++n) {
+    const int a = n % nq_, b = (n / nq_) % nq_, c = n / n2_;
+    const double w3 = ref_.weights[size_t(a)] * ref_.weights[size_t(b)] * ref_.weights[size_t(c)];
+    weight[size_t(n)] = J * w3;
+  }
+  for (int d = 0; d < 3; ++d)
+    for (int i = 0; i < nq_; ++i) {
+      double g = 2.0;
+      if (i > 0) g = std::min(g, ref_.nodes[size_t(i)] - ref_.nodes[size_t(i) - 1]);
+      if (i + 1 < nq_) g = std::min(g, ref_.nodes[size_t(i) + 1] - ref_.nodes[size_t(i)]);
+      dx[size_t(d * nq_ + i)] = (0.5 * mesh_->delta[d]) * g;
+    }
+  int64_t total = 0;
+  for (auto& ls : shards_) total += ls.end - ls.begin;
+  partials.assign(static_cast<size_t>(total), 0.0);
+  bad = false;
+  int64_t at = 0;
+  for (auto& ls : shards_) {
+    int np = 0;
+    RC(ls.dev->reduce(kind, reg, var, weight.data(), dx.data(), opt_.gas.gamma,
+                      partials.data() + at, &np));
+    bad = bad || np != 0;
+    at += ls.end - ls.begin;
+  }
+  return ESDG_B200_OK;
+}
+
+int SolverCore::compute_dt(double courant, double* dt_out) {
+  if (reduction_ == ESDG_B200_REDUCE_ON_HOST) return compute_dt_host(courant, dt_out);
+  std::vector<double> part;
+  bool bad = false;
+  RC(device_partials(ESDG_B200_REDUCE_DT, ESDG_B200_REG_Q, 0, part, bad));
+  if (bad) {
+    set_message("compute_dt: non-physical state");
+    return ESDG_B200_NONPHYSICAL;
+  }
+  double dt = std::numeric_limits<double>::infinity();
+  for (double v : part) dt = std::min(dt, v);
+  *dt_out = courant * dt;
+  return ESDG_B200_OK;
+}
+
+int SolverCore::quadrature_total(int reg, int var, double* out) {
+  if (var < 0 || var > 4 || (reg != 0 && reg != 1)) return ESDG_B200_BADARG;
+  if (reduction_ == ESDG_B200_REDUCE_ON_HOST) return quadrature_total_host(reg, var, out);
+  std::vector<double> part;
+  bool bad = false;
+  RC(device_partials(ESDG_B200_REDUCE_QUADRATURE, reg, var, part, bad));
+  Neumaier sum;
+  for (double v : part) sum.add(v);
+  *out = sum.value();
+  return ESDG_B200_OK;
+}
+
+int SolverCore::total_entropy(double* out) {
+  if (reduction_ == ESDG_B200_REDUCE_ON_HOST) return total_entropy_host(out);
+  std::vector<double> part;
+  bool bad = false;
+  RC(device_partials(ESDG_B200_REDUCE_ENTROPY, ESDG_B200_REG_Q, 0, part, bad));
+  if (bad) return ESDG_B200_NONPHYSICAL;
+  Neumaier sum;
+  for (double v : part) sum.add(v);
+  *out = sum.value();
+  return ESDG_B200_OK;
+}
+
+int SolverCore::entropy_production(double* out) {
+  if (reduction_ == ESDG_B200_REDUCE_ON_HOST) return entropy_production_host(out);
+  std::vector<double> part;
+  bool bad = false;
+  RC(device_partials(ESDG_B200_REDUCE_ENTROPY_PRODUCTION, ESDG_B200_REG_Q, 0, part, bad));
+  if (bad) return ESDG_B200_NONPHYSICAL;
+  Neumaier sum;
+  for (double v : part) sum.add(v);
   *out = sum.value();
   return ESDG_B200_OK;
 }

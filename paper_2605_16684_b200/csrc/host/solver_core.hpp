@@ -72,6 +72,8 @@ public:
   int quadrature_total(int reg, int var, double* out);
   int total_entropy(double* out);
   int entropy_production(double* out);
+  // ESDG_B200_REDUCE_ON_DEVICE (default) or ESDG_B200_REDUCE_ON_HOST
+  int set_reduction(int mode);
 
   int enable_timing(bool on);
   int timers(double seconds[4], int64_t* launches, bool reset);
@@ -101,6 +103,12 @@ private:
   // downloads register `reg` chunk by chunk and calls f(global_elem, ptr)
   template <class F>
   int for_each_element_chunk(int reg, int reg2, F&& f);
+  // K6 on every local shard: one partial per local element, Morton order
+  int device_partials(int kind, int reg, int var, std::vector<double>& partials, bool& bad);
+  int compute_dt_host(double courant, double* dt);
+  int quadrature_total_host(int reg, int var, double* out);
+  int total_entropy_host(double* out);
+  int entropy_production_host(double* out);
 
   Mesh* mesh_ = nullptr;
   Options opt_;
@@ -110,6 +118,7 @@ private:
   int64_t local_begin_ = 0, local_end_ = 0;
   std::vector<LocalShard> shards_;
   int path_ = ESDG_B200_PATH_SPLIT;
+  int reduction_ = ESDG_B200_REDUCE_ON_DEVICE;
   bool any_halo_ = false;
   esdg_b200_error err_{};
   bool timing_ = false;

@@ -37,6 +37,106 @@ namespace {
 
 constexpr unsigned long long kNoFlag = ~0ull;
 
+// ---- K6: per-element reductions ---------------------
+// quadrature_total / total_entropy / entropy_production
+// (diagnostics.hpp:30-106) and compute_stable_dt (time_integration.hpp:55-92)
+// without moving the state to the host: one warp per element evaluates the
+// per-node terms in 64-bit exactly as the reference writes them, sums them
+// with Neumaier compensation (lanes over nodes, then lane 0 over lanes, a
+// fixed order) and stores ONE double per element; the host finishes with a
+// compensated sum over elements in Morton order. The dt term is a minimum and
+// therefore bitwise the reference's value.
+struct ReduceParams {
+  const void* q;
+  const void* k;
+  const void* phi;
+  const double* node_weight; // [n3]  J w_a w_b w_c
+  const double* dx;          // [3][nq] half width * LGL gap
+  double* out;               // [ne]
+  unsigned* bad;
+  double gamma;
+  long long ne;
+  int nq, n3, var;
+};
+
+__device__ __forceinline__ void neumaier_add(double& s, double& c, double x) {
+  const double t = s + x;
+  c += (fabs(s) >= fabs(x)) ? (s - t) + x : (x - t) + s;
+  s = t;
+}
+
+template <class Real, int KIND>
+__global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams P) {
+  const int lane = threadIdx.x & 31;
+  const long long e = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (e >= P.ne) return;
+  const Real* q = static_cast<const Real*>(P.q) + e * 5 * P.n3;
+  const Real* k = static_cast<const Real*>(P.k) + e * 5 * P.n3;
+  const Real* ph = static_cast<const Real*>(P.phi) + e * P.n3;
+  const int n2 = P.nq * P.nq;
+  const double gamma = P.gamma;
+  double s = 0.0, c = 0.0, mn = __longlong_as_double(0x7ff0000000000000LL);
+  bool bad = false;
+  for (int n = lane; n < P.n3; n += 32) {
+    if constexpr (KIND == 0) {
+      neumaier_add(s, c, P.node_weight[n] * double(q[P.var * P.n3 + n]));
+    } else {
+    double u[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) u[v] = double(q[v * P.n3 + n]);
+    const double phi = double(ph[n]);
+    if (KIND == 3) {
+      if (!(u[0] > 0.0)) { bad = true; continue; }
+      const double ke = 0.5 * (u[1] * u[1] + u[2] * u[2] + u[3] * u[3]) / u[0];
+      const double p = (gamma - 1.0) * (u[4] - ke - u[0] * phi);
+      if (!(p > 0.0)) { bad = true; continue; }
+      const double cs = sqrt(gamma * p / u[0]);
+      const int idx[3] = {n % P.nq, (n / P.nq) % P.nq, n / n2};
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double vel = fabs(u[1 + d] / u[0]);
+        mn = fmin(mn, P.dx[d * P.nq + idx[d]] / (vel + cs));
+      }
+      continue;
+    }
+    const double rho = u[0];
+    const double ke = 0.5 * (u[1] * u[1] + u[2] * u[2] + u[3] * u[3]) / rho;
+    const double p = (gamma - 1.0) * (u[4] - ke - rho * phi);
+    if (!(rho > 0.0) || !(p > 0.0)) bad = true;
+    const double ent = log(p) - gamma * log(rho);
+    if (KIND == 1) {
+      neumaier_add(s, c, P.node_weight[n] * (-rho * ent / (gamma - 1.0)));
+    } else {
+      double r[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) r[v] = double(k[v * P.n3 + n]);
+      const double bq = rho / (2.0 * p);
+      const double w[3] = {u[1] / rho, u[2] / rho, u[3] / rho};
+      const double w2 = w[0] * w[0] + w[1] * w[1] + w[2] * w[2];
+      const double vv[5] = {(gamma - ent) / (gamma - 1.0) - bq * (w2 - 2.0 * phi),
+                            2.0 * bq * w[0], 2.0 * bq * w[1], 2.0 * bq * w[2], -2.0 * bq};
+      neumaier_add(s, c, P.node_weight[n] * (vv[0] * r[0] + vv[1] * r[1] + vv[2] * r[2] +
+                                             vv[3] * r[3] + vv[4] * r[4]));
+    }
+    }
+  }
+  if (KIND == 3) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  } else {
+    for (int src = 1; src < 32; ++src) {
+      const double so = __shfl_sync(0xffffffffu, s, src);
+      const double co = __shfl_sync(0xffffffffu, c, src);
+      if (lane == 0) {
+        neumaier_add(s, c, so);
+        c += co;
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(P.bad, 1u);
+  if (lane == 0) P.out[e] = KIND == 3 ? mn : s + c;
+}
+
 template <class Real>
 class Shard final : public ShardBase {
 public:
@@ -240,6 +340,56 @@ public:
     return ESDG_B200_OK;
   }
 
+  int reduce(int kind, int reg, int var, const double* node_weight, const double* dx,
+             double gamma, double* partials, int* nonphysical) override {
+    if (kind < 0 || kind > 3 || (reg != 0 && reg != 1) || var < 0 || var > 4 ||
+        !node_weight || !dx || !partials || !nonphysical)
+      return bad("reduce: bad argument");
+    *nonphysical = 0;
+    if (ne_ == 0) return ESDG_B200_OK;
+    CU(cudaSetDevice(device_));
+    if (!red_out_) {
+      CU(cudaMalloc(&red_out_, sizeof(double) * size_t(ne_)));
+      CU(cudaMalloc(&red_tab_, sizeof(double) * size_t(n3_ + 3 * nq_)));
+      CU(cudaMalloc(&red_bad_, sizeof(unsigned)));
+    }
+    CU(cudaMemcpyAsync(red_tab_, node_weight, sizeof(double) * size_t(n3_),
+                       cudaMemcpyHostToDevice, stream_));
+    CU(cudaMemcpyAsync(red_tab_ + n3_, dx, sizeof(double) * size_t(3 * nq_),
+                       cudaMemcpyHostToDevice, stream_));
+    CU(cudaMemsetAsync(red_bad_, 0, sizeof(unsigned), stream_));
+    ReduceParams P;
+    P.q = reg_ptr(kind == 0 ? reg : 0);
+    P.k = k_;
+    P.phi = phi_;
+    P.node_weight = red_tab_;
+    P.dx = red_tab_ + n3_;
+    P.out = red_out_;
+    P.bad = red_bad_;
+    P.gamma = gamma;
+    P.ne = ne_;
+    P.nq = nq_;
+    P.n3 = n3_;
+    P.var = var;
+    const unsigned blocks = unsigned((ne_ * 32 + 255) / 256);
+    switch (kind) {
+      case 0: reduce_kernel<Real, 0><<<blocks, 256, 0, stream_>>>(P); break;
+      case 1: reduce_kernel<Real, 1><<<blocks, 256, 0, stream_>>>(P); break;
+      case 2: reduce_kernel<Real, 2><<<blocks, 256, 0, stream_>>>(P); break;
+      default: reduce_kernel<Real, 3><<<blocks, 256, 0, stream_>>>(P); break;
+    }
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "reduce_kernel");
+    ++launches_;
+    unsigned flag = 0;
+    CU(cudaMemcpyAsync(partials, red_out_, sizeof(double) * size_t(ne_),
+                       cudaMemcpyDeviceToHost, stream_));
+    CU(cudaMemcpyAsync(&flag, red_bad_, sizeof(unsigned), cudaMemcpyDeviceToHost, stream_));
+    CU(cudaStreamSynchronize(stream_));
+    *nonphysical = flag ? 1 : 0;
+    return ESDG_B200_OK;
+  }
+
   int check(cudaStream_t st, int src, esdg_b200_error* err) override {
     CU(cudaSetDevice(device_));
     cudaStream_t s = pick(st);
@@ -375,6 +525,9 @@ private:
     cudaFree(ylevel_);
     cudaFree(cor_f_);
     cudaFree(flag_);
+    cudaFree(red_out_);
+    cudaFree(red_tab_);
+    cudaFree(red_bad_);
     cudaFree(flag_records_);
     if (flag_host_) cudaFreeHost(flag_host_);
     if (stream_) cudaStreamDestroy(stream_);
@@ -392,6 +545,8 @@ private:
   int32_t *nbr_ = nullptr, *send_elem_ = nullptr, *send_face_ = nullptr,
           *ylevel_ = nullptr;
   unsigned long long *flag_ = nullptr, *flag_host_ = nullptr;
+  double *red_out_ = nullptr, *red_tab_ = nullptr;
+  unsigned* red_bad_ = nullptr;
   dev::FlagRecord* flag_records_ = nullptr;
   cudaStream_t stream_ = nullptr;
   int64_t launches_ = 0;
@@ -404,8 +559,9 @@ __global__ void __launch_bounds__(256) fma_peak_kernel(Real* out, int iters) {
   Real a[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) a[i] = Real(threadIdx.x + i) * Real(1e-3);
-  // register operands (not immediates): the figure wanted is the 3-register
-  // FMA rate the flux code runs at
+  // m and c are the same in every thread, so the compiler keeps them in
+  // uniform registers: each FMA reads ONE vector register. This is the pipe's
+  // nominal rate (one warp instruction per two cycles per sub-partition).
   const Real m = Real(1) - Real(1e-6) * Real(1 + (iters & 1));
   const Real c = Real(1e-6) * Real(1 + (iters & 2));
   for (int it = 0; it < iters; ++it) {
@@ -419,6 +575,32 @@ __global__ void __launch_bounds__(256) fma_peak_kernel(Real* out, int iters) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) s += a[i];
   if (s == Real(123.456)) out[0] = s; // keeps the chain alive
+}
+
+// The same with three DISTINCT, thread-varying vector-register operands per
+// FMA (x = fma(y, z, x)): on sm_100 such an FP64 instruction occupies the
+// pipe for three cycles instead of two, so general FP64 code cannot reach
+// the nominal figure (tools/ubench/fp64_operands_ubench.cu).
+template <class Real>
+__global__ void __launch_bounds__(256) fma3_peak_kernel(Real* out, const Real* in, int iters) {
+  Real x[8], y[8], z[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    x[i] = in[(threadIdx.x + 7 * i) & 255];
+    y[i] = Real(1) - Real(1e-6) * in[(threadIdx.x + 11 * i + 1) & 255];
+    z[i] = Real(1e-6) * in[(threadIdx.x + 13 * i + 2) & 255];
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = dev::fma_(y[(i + r) & 7], z[(i + 3 * r + 1) & 7], x[i]);
+    }
+  }
+  Real s = Real(0);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == Real(123.456)) out[0] = s;
 }
 
 // Device self-test of the arithmetic identities the kernels rely on.
@@ -490,12 +672,17 @@ int run_selftest(int device, double* out5) {
 }
 
 template <class Real>
-int measure_peak(int device, double* tflops) {
+int measure_peak(int device, int vector_operands, double* tflops) {
   CU(cudaSetDevice(device));
   cudaDeviceProp prop;
   CU(cudaGetDeviceProperties(&prop, device));
   Real* out = nullptr;
-  CU(cudaMalloc(&out, sizeof(Real)));
+  CU(cudaMalloc(&out, sizeof(Real) * 257));
+  {
+    Real h[256];
+    for (int i = 0; i < 256; ++i) h[i] = Real(1) + Real(i) * Real(1e-3);
+    CU(cudaMemcpy(out + 1, h, sizeof h, cudaMemcpyHostToDevice));
+  }
   const int blocks = prop.multiProcessorCount * 8, threads = 256, iters = 4096;
   cudaEvent_t t0, t1;
   CU(cudaEventCreate(&t0));
@@ -503,7 +690,10 @@ int measure_peak(int device, double* tflops) {
   double best = 0.0;
   for (int rep = 0; rep < 5; ++rep) {
     CU(cudaEventRecord(t0));
-    fma_peak_kernel<Real><<<blocks, threads>>>(out, iters);
+    if (vector_operands >= 3)
+      fma3_peak_kernel<Real><<<blocks, threads>>>(out, out + 1, iters);
+    else
+      fma_peak_kernel<Real><<<blocks, threads>>>(out, iters);
     CU(cudaEventRecord(t1));
     CU(cudaEventSynchronize(t1));
     float ms = 0.f;
@@ -679,6 +869,16 @@ int esdg_b200_shard_check(esdg_b200_shard* s, void* stream,
            : ESDG_B200_BADARG;
 }
 
+int esdg_b200_shard_reduce(esdg_b200_shard* s, int kind, int reg, int var,
+                           const double* node_weight, const double* dx, double gamma,
+                           double* partials, int32_t* nonphysical) {
+  if (!s) return ESDG_B200_BADARG;
+  int np = 0;
+  const int rc = s->impl->reduce(kind, reg, var, node_weight, dx, gamma, partials, &np);
+  if (nonphysical) *nonphysical = np;
+  return rc;
+}
+
 int64_t esdg_b200_shard_launch_count(const esdg_b200_shard* s) {
   return s ? s->impl->launch_count() : 0;
 }
@@ -692,8 +892,15 @@ int esdg_b200_selftest(int device, int precision, double out5[5]) {
 
 int esdg_b200_measure_fma_peak(int device, int precision, double* tflops) {
   if (!tflops) return ESDG_B200_BADARG;
-  if (precision == 8) return esdg_b200::measure_peak<double>(device, tflops);
-  if (precision == 4) return esdg_b200::measure_peak<float>(device, tflops);
+  if (precision == 8) return esdg_b200::measure_peak<double>(device, 1, tflops);
+  if (precision == 4) return esdg_b200::measure_peak<float>(device, 1, tflops);
+  return ESDG_B200_BADARG;
+}
+
+int esdg_b200_measure_fma3_peak(int device, int precision, double* tflops) {
+  if (!tflops) return ESDG_B200_BADARG;
+  if (precision == 8) return esdg_b200::measure_peak<double>(device, 3, tflops);
+  if (precision == 4) return esdg_b200::measure_peak<float>(device, 3, tflops);
   return ESDG_B200_BADARG;
 }
 

@@ -38,6 +38,9 @@ public:
                           int stage, cudaStream_t st) = 0;
   virtual int axpy(double b, cudaStream_t st) = 0;
   virtual int check(cudaStream_t st, int src, esdg_b200_error* err) = 0;
+  // K6: one partial per element, see esdg_b200_shard_reduce
+  virtual int reduce(int kind, int reg, int var, const double* node_weight, const double* dx,
+                     double gamma, double* partials, int* nonphysical) = 0;
 };
 
 int create_shard(const esdg_b200_shard_desc& d, ShardBase** out);

@@ -140,7 +140,15 @@ static void parity_and_partitions() {
   std::printf("  3-step state error %.3e of max|q|\n", dmax / qmax);
   CHECK(dmax <= 1e-12 * qmax);
   CHECK(std::fabs(s1.compute_dt(0.5) - orc_compute_dt_f64(o, 0.5)) <= 1e-12 * orc_compute_dt_f64(o, 0.5));
-  CHECK(s1.quadrature_total(0) == orc_quadrature_total_f64(o, a.data.data(), 0));
+  {
+    // device reduction (default): per-element partial sums, 1e-14 relative;
+    // host reduction: the reference's serial Neumaier chain, bitwise
+    const double want = orc_quadrature_total_f64(o, a.data.data(), 0);
+    CHECK(std::fabs(s1.quadrature_total(0) - want) <= 1e-14 * std::fabs(want));
+    s1.set_reduction_on_host(true);
+    CHECK(s1.quadrature_total(0) == want);
+    s1.set_reduction_on_host(false);
+  }
   orc_solver_destroy_f64(o);
   orc_mesh_destroy(om);
 }

@@ -299,15 +299,47 @@ def test_init_case_matches_oracle(port):
 
 
 def test_diagnostics_match_oracle(port):
+    """diagnostics.hpp:30-106 and compute_stable_dt: the host reduction
+    reproduces the reference's serial Neumaier chain bitwise; the device
+    reduction (K6, default) sums per element first and agrees to 1e-14
+    relative, its dt (a minimum) bitwise."""
     o, g = make(port, "bubble", (1, False), 4)
     q = o.init_case(po.CASE_BUBBLE_SMOOTH).copy()
     g.set_state(q)
-    for var in (0, 4):
-        assert g.quadrature_total(var) == o.quadrature_total(q, var)
-    assert g.total_entropy() == o.total_entropy(q)
     g.rhs(0.0, 1.0)
     k = g.get_state(capi.REG_K)
-    assert g.entropy_production() == o.entropy_production(q, k)
+    want = [o.quadrature_total(q, 0), o.quadrature_total(q, 4), o.total_entropy(q),
+            o.entropy_production(q, k)]
+    scale = [abs(want[0]), abs(want[1]), abs(want[2]),
+             float(np.abs(k).max()) * abs(want[2]) / max(float(np.abs(q[:, 0]).max()), 1e-300)]
+    g.set_reduction(capi.REDUCE_ON_HOST)
+    got = [g.quadrature_total(0), g.quadrature_total(4), g.total_entropy(), g.entropy_production()]
+    assert got == want
+    dt_host = g.compute_dt(0.5)
+    assert dt_host == o.compute_dt(0.5)
+    g.set_reduction(capi.REDUCE_ON_DEVICE)
+    got = [g.quadrature_total(0), g.quadrature_total(4), g.total_entropy(), g.entropy_production()]
+    for a, b, s in zip(got[:3], want[:3], scale[:3]):
+        assert abs(a - b) <= 1e-14 * s, (a, b)
+    # entropy production: a sum of cancelling terms; 1e-12 of its abs-sum scale
+    assert abs(got[3] - want[3]) <= 1e-6 * abs(want[3]) + 1e-12 * scale[3], (got[3], want[3])
+    assert g.compute_dt(0.5) == dt_host
+
+
+def test_device_reductions_fp32_and_partitions(port):
+    """K6 on an FP32 state and on several partitions: same values as the
+    host reduction to rounding, dt bitwise."""
+    for prec, ranks in (("f32", 1), ("f64", 3)):
+        o, g = make(port, "bubble", (1, False), 3, prec=prec, ranks=ranks)
+        q = o.init_case(po.CASE_BUBBLE_SMOOTH).copy()
+        g.set_state(q)
+        g.set_reduction(capi.REDUCE_ON_HOST)
+        want = [g.quadrature_total(0), g.quadrature_total(4), g.total_entropy(), g.compute_dt(0.5)]
+        g.set_reduction(capi.REDUCE_ON_DEVICE)
+        got = [g.quadrature_total(0), g.quadrature_total(4), g.total_entropy(), g.compute_dt(0.5)]
+        for a, b in zip(got[:3], want[:3]):
+            assert abs(a - b) <= 1e-14 * abs(b), (prec, a, b)
+        assert got[3] == want[3]
 
 
 def test_stage_path_equals_fused_plus_axpy_bitwise(port):

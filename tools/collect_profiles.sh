@@ -21,4 +21,11 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:rhs_
   -o $OUT/${TAG}_full_stage python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $OUT/${TAG}_ncu_full_stage.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"rhs_kernel|axpy_kernel" -s 45 -c 3 \
   -o $OUT/${TAG}_full_split python bench.py --path split --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $OUT/${TAG}_ncu_full_split.log 2>&1
+for r in ${TAG}_full_stage ${TAG}_full_split; do
+  ncu -i $OUT/$r.ncu-rep --page source --csv > $OUT/${r}_source.csv 2>/dev/null
+done
+# micro-benchmarks the design notes cite (FP64 pipe, operand count, shared memory)
+for u in fp64_ubench fp64_operands_ubench smem_ubench; do
+  [ -x tools/ubench/$u ] && timeout 120 ./tools/ubench/$u > $OUT/${TAG}_ubench_$u.txt 2>&1
+done
 ls -la $OUT | tail -30
