@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   store_log_table(logtab, ltab, tid, EPB * N2);
   if (sizeof(Real) == 8) __syncthreads();
   if (active) {
-    if (SURF) { // the first direction's neighbour traces: they land during the logs
+    if (SURF && !VOL) { // surface-only kernel: registers to spare, fetch early
       fetch(0, cur[0]);
       fetch(1, cur[1]);
     }
@@ -480,6 +480,13 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
       for (int j = 0; j < V_COUNT; ++j) vals[j * VS + s] = nvs[k][j];
     }
     const int bad = badmask ? __ffs(badmask) - 1 : -1;
+    if (SURF && VOL) {
+      // the first direction's neighbour traces: issued here, not before the
+      // logarithms (26 registers the fused kernel's node loop cannot spare);
+      // they land while the CTA gathers at the barrier
+      fetch(0, cur[0]);
+      fetch(1, cur[1]);
+    }
     if (bad >= 0) {
       const Real* qb = qe + bad * N2;
       Real qq[5], nv[V_COUNT], pr;
