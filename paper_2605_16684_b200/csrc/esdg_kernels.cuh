@@ -769,7 +769,7 @@ template <> struct Tile<4, 8> { static constexpr int EPB = 8, MINB = 3; };
 template <> struct Tile<5, 8> { static constexpr int EPB = ESDG_TUNE_EPB, MINB = ESDG_TUNE_MINB; };
 template <> struct Tile<6, 8> { static constexpr int EPB = 3, MINB = 2; };
 template <> struct Tile<7, 8> { static constexpr int EPB = 2, MINB = 2; };
-template <> struct Tile<8, 8> { static constexpr int EPB = 2, MINB = 1; };
+template <> struct Tile<8, 8> { static constexpr int EPB = 1, MINB = 3; };
 template <> struct Tile<2, 4> { static constexpr int EPB = 32, MINB = 4; };
 template <> struct Tile<3, 4> { static constexpr int EPB = 14, MINB = 4; };
 template <> struct Tile<4, 4> { static constexpr int EPB = 8, MINB = 4; };
