@@ -236,54 +236,22 @@ struct NbrRaw {
 //   otherwise: n (S - G' b-/b+ e_n) + D(nbr,own)/2 = the same expression,
 // so the orientation never has to be looked at, and the two sides of a face
 // subtract exactly opposite numbers: conservation is exact.
-template <class Real, int NQ>
-__device__ __forceinline__ void face_contribution(const RhsParams<Real, NQ>& P,
-                                                  const Node<Real>& own,
-                                                  const NbrRaw<Real>& nbr, int dir,
-                                                  int side, long long eg, int fn,
-                                                  const Real* logtab, Real c[5]) {
-  Node<Real> nb;
-  if (nbr.code == -1) {
-    // reflecting wall: mirror state, phi+ = phi- (kernels.hpp:364-367)
-    nb = own;
-    nb.hun = -own.hun;
-  } else {
-    Real nv[V_COUNT], pr;
-    if (!node_vals(nbr.q, nbr.ph, P.gas.gm1, logtab, nv, pr))
-      raise_flag(P.flag, P.flag_records, P.stage, 1, P.elem_offset + eg, fn,
-                 double(nbr.q[0]), double(pr));
-    nb = rotate_node(nv, dir);
-  }
-  const PairFlux<Real> pf = pair_flux(own, nb, P.gas.cg);
-  Real dd[5] = {Real(0), Real(0), Real(0), Real(0), Real(0)};
-  if (P.dissipation) matrix_dissipation(own, nb, pf.rho_log, pf.inv_blog, P.gas, dd);
-  Real fo[5];
-  point_flux(own, P.gas.cg, fo);
-  // commit_face_side (kernels.hpp:391-430)
-  const Real n_own = side ? Real(1) : Real(-1);
-  const Real g_own = pf.tg * own.hib;
-  const Real lift = P.lift[dir];
-  const Real phi_own = own.hphi + own.hphi;
-  Real fl[5];
-  fl[0] = n_own * pf.f[0] - Real(0.5) * dd[0];
-  fl[1] = n_own * pf.f[1] + n_own * g_own - Real(0.5) * dd[1];
-  fl[2] = n_own * pf.f[2] - Real(0.5) * dd[2];
-  fl[3] = n_own * pf.f[3] - Real(0.5) * dd[3];
-  fl[4] = n_own * pf.f[4] - Real(0.5) * fma_(phi_own, dd[0], dd[4]);
-#pragma unroll
-  for (int v = 0; v < 5; ++v) c[v] = lift * (fl[v] - n_own * fo[v]);
-}
-
 // The two faces of one direction (side 0 at node 0, side 1 at node NQ-1 of
 // the line through the face node) share no data, so their evaluations are
 // written stage by stage: two independent dependency chains for the
-// scheduler instead of one. Same arithmetic as face_contribution per face.
+// scheduler instead of one.
+// Split in two so that the caller can start the next direction's gather as
+// soon as the raw traces have been consumed.
+//
+// Part 1: node values of the two neighbour traces. A reflecting wall arrives
+// here as the element's own trace with the normal momentum negated (see
+// fetch): compute_node_vals of that is bitwise the own node with hun negated,
+// i.e. mirror_state with phi+ = phi- (kernels.hpp:364-367, physics.hpp:309-313).
 template <class Real, int NQ>
-__device__ __forceinline__ void face_pair_contribution(const RhsParams<Real, NQ>& P,
-                                                       const Node<Real> (&own)[2],
-                                                       const NbrRaw<Real> (&nbr)[2], int dir,
-                                                       long long eg, int fn,
-                                                       const Real* logtab, Real (&c)[2][5]) {
+__device__ __forceinline__ void face_pair_neighbours(const RhsParams<Real, NQ>& P,
+                                                     const NbrRaw<Real> (&nbr)[2], int dir,
+                                                     long long eg, int fn, const Real* logtab,
+                                                     Node<Real> (&nb)[2]) {
   Real q2[2][5], ph2[2], nv[2][V_COUNT], pr[2];
 #pragma unroll
   for (int f = 0; f < 2; ++f) {
@@ -292,20 +260,21 @@ __device__ __forceinline__ void face_pair_contribution(const RhsParams<Real, NQ>
     ph2[f] = nbr[f].ph;
   }
   const unsigned bad = node_vals_line<Real, 2>(q2, ph2, P.gas.gm1, logtab, nv, pr);
-  Node<Real> nb[2];
 #pragma unroll
   for (int f = 0; f < 2; ++f) {
     nb[f] = rotate_node(nv[f], dir);
-    if (nbr[f].code == -1) {
-      // reflecting wall: mirror state, phi+ = phi- (kernels.hpp:364-367); the
-      // values computed from the placeholder trace are discarded
-      nb[f] = own[f];
-      nb[f].hun = -own[f].hun;
-    } else if (bad & (1u << f)) {
+    if (bad & (1u << f))
       raise_flag(P.flag, P.flag_records, P.stage, 1, P.elem_offset + eg, fn,
                  double(q2[f][0]), double(pr[f]));
-    }
   }
+}
+
+// Part 2: fluxes, dissipation and lift of the two faces.
+template <class Real, int NQ>
+__device__ __forceinline__ void face_pair_contribution(const RhsParams<Real, NQ>& P,
+                                                       const Node<Real> (&own)[2],
+                                                       const Node<Real> (&nb)[2], int dir,
+                                                       Real (&c)[2][5]) {
   PairFlux<Real> pf[2];
 #pragma unroll
   for (int f = 0; f < 2; ++f) pf[f] = pair_flux(own[f], nb[f], P.gas.cg);
@@ -378,7 +347,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // Neighbour state of face lf, fetched one face ahead of its use so the
   // (mostly L2-resident) gather hides behind arithmetic. The six neighbour
   // codes were read at kernel start, so a fetch is one round trip, not two.
-  NbrRaw<Real> cur[2], nxt[2];
+  NbrRaw<Real> cur[2];
   auto fetch = [&](int lf, NbrRaw<Real>& r) {
     const int dir = lf >> 1, side = lf & 1;
     const int d1 = dir == 2 ? 0 : dir + 1;
@@ -399,10 +368,16 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
       for (int v = 0; v < 5; ++v) r.q[v] = P.ghost_q[(g * 5 + v) * N2 + l];
       r.ph = P.ghost_phi[g * N2 + l];
     } else {
-      // reflecting wall: no trace; a harmless placeholder state
+      // reflecting wall (mirror_state, physics.hpp:309-313): the element's own
+      // trace with the normal momentum negated, phi+ = phi-
+      const int n_own = (side ? NQ - 1 : 0) * gpitch(dir) + l0 * gpitch(d1) + l1 * gpitch(d2);
+      const Real* qo = P.q + eg * (5 * N3);
 #pragma unroll
-      for (int v = 0; v < 5; ++v) r.q[v] = Real(v == 0 || v == 4);
-      r.ph = Real(0);
+      for (int v = 0; v < 5; ++v) {
+        const Real x = qo[v * N3 + n_own];
+        r.q[v] = (v == 1 + dir) ? -x : x;
+      }
+      r.ph = P.phi[eg * N3 + n_own];
     }
   };
 
@@ -508,12 +483,17 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
 #pragma unroll 1
     for (int dir = 0; dir < 3; ++dir) {
       if (active) {
-        if (dir < 2) {
-          fetch(2 * dir + 2, nxt[0]);
-          fetch(2 * dir + 3, nxt[1]);
-        }
         const int d1 = dir == 2 ? 0 : dir + 1;
         const int d2 = d1 == 2 ? 0 : d1 + 1;
+        // node values of the two neighbour traces, then -- the raw traces are
+        // dead -- the next direction's gather into the same registers; it
+        // lands while this direction's fluxes are evaluated
+        Node<Real> nb[2];
+        face_pair_neighbours<Real, NQ>(P, cur, dir, eg, l, logtab, nb);
+        if (dir < 2) {
+          fetch(2 * dir + 2, cur[0]);
+          fetch(2 * dir + 3, cur[1]);
+        }
         // FaceIndexer::node (mesh.hpp:107-114): tangential axes d1, d2
         const int s0 = e * N3P + l0 * spitch(d1) + l1 * spitch(d2);
         const int s_own[2] = {s0, s0 + (NQ - 1) * spitch(dir)};
@@ -521,7 +501,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         own[0] = load_node(vals, VS, s_own[0], dir);
         own[1] = load_node(vals, VS, s_own[1], dir);
         Real c[2][5], o[2][5];
-        face_pair_contribution<Real, NQ>(P, own, cur, dir, eg, l, logtab, c);
+        face_pair_contribution<Real, NQ>(P, own, nb, dir, c);
         Real* tn = tend + (1 + dir) * VS;
         Real* tt1 = tend + (1 + d1) * VS;
         Real* tt2 = tend + (1 + d2) * VS;
@@ -542,8 +522,6 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           tt2[s_own[f]] = fma_(-P.gain, c[f][3], o[f][3]);
           t4[s_own[f]] = fma_(-P.gain, c[f][4], o[f][4]);
         }
-        cur[0] = nxt[0];
-        cur[1] = nxt[1];
       }
       __syncthreads();
     }
