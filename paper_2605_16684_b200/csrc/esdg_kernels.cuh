@@ -190,6 +190,28 @@ __device__ __forceinline__ void sweep_line(const RhsParams<Real, NQ>& P,
 #pragma unroll
     for (int v = 0; v < 5; ++v) acc[i][v] = fma_(cii, f[v], acc[i][v]);
   }
+#ifdef ESDG_LADDER_NO_SYMMETRY
+  // Ladder rung without pair symmetry (the reference's "logmean" variant,
+  // kernels.hpp:27-34): every ORDERED pair is evaluated and only node i is
+  // updated. Build-time switch for the measurement in profiles/; the product
+  // always uses the symmetric sweep below.
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) {
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+      if (j == i) continue;
+      const PairFlux<Real> pf = pair_flux(nd[i], nd[j], P.gas.cg);
+      const Real cij = P.negd[i * NQ + j];
+      const Real fni = fma_(pf.tg, nd[i].hib, pf.f[1]);
+      acc[i][0] = fma_(cij, pf.f[0], acc[i][0]);
+      acc[i][1] = fma_(cij, fni, acc[i][1]);
+      acc[i][2] = fma_(cij, pf.f[2], acc[i][2]);
+      acc[i][3] = fma_(cij, pf.f[3], acc[i][3]);
+      acc[i][4] = fma_(cij, pf.f[4], acc[i][4]);
+    }
+  }
+  return;
+#endif
   // off-diagonal pairs, each once (kernels.hpp:190-231)
 #pragma unroll
   for (int i = 0; i < NQ; ++i) {
@@ -247,21 +269,21 @@ struct NbrRaw {
 // here as the element's own trace with the normal momentum negated (see
 // fetch): compute_node_vals of that is bitwise the own node with hun negated,
 // i.e. mirror_state with phi+ = phi- (kernels.hpp:364-367, physics.hpp:309-313).
-template <class Real, int NQ>
+template <class Real, int NQ, int F>
 __device__ __forceinline__ void face_pair_neighbours(const RhsParams<Real, NQ>& P,
-                                                     const NbrRaw<Real> (&nbr)[2], int dir,
+                                                     const NbrRaw<Real> (&nbr)[F], int dir,
                                                      long long eg, int fn, const Real* logtab,
-                                                     Node<Real> (&nb)[2]) {
-  Real q2[2][5], ph2[2], nv[2][V_COUNT], pr[2];
+                                                     Node<Real> (&nb)[F]) {
+  Real q2[F][5], ph2[F], nv[F][V_COUNT], pr[F];
 #pragma unroll
-  for (int f = 0; f < 2; ++f) {
+  for (int f = 0; f < F; ++f) {
 #pragma unroll
     for (int v = 0; v < 5; ++v) q2[f][v] = nbr[f].q[v];
     ph2[f] = nbr[f].ph;
   }
-  const unsigned bad = node_vals_line<Real, 2>(q2, ph2, P.gas.gm1, logtab, nv, pr);
+  const unsigned bad = node_vals_line<Real, F>(q2, ph2, P.gas.gm1, logtab, nv, pr);
 #pragma unroll
-  for (int f = 0; f < 2; ++f) {
+  for (int f = 0; f < F; ++f) {
     nb[f] = rotate_node(nv[f], dir);
     if (bad & (1u << f))
       raise_flag(P.flag, P.flag_records, P.stage, 1, P.elem_offset + eg, fn,
@@ -270,31 +292,31 @@ __device__ __forceinline__ void face_pair_neighbours(const RhsParams<Real, NQ>& 
 }
 
 // Part 2: fluxes, dissipation and lift of the two faces.
-template <class Real, int NQ>
+template <class Real, int NQ, int F>
 __device__ __forceinline__ void face_pair_contribution(const RhsParams<Real, NQ>& P,
-                                                       const Node<Real> (&own)[2],
-                                                       const Node<Real> (&nb)[2], int dir,
-                                                       Real (&c)[2][5]) {
-  PairFlux<Real> pf[2];
+                                                       const Node<Real> (&own)[F],
+                                                       const Node<Real> (&nb)[F], int dir,
+                                                       int side0, Real (&c)[F][5]) {
+  PairFlux<Real> pf[F];
 #pragma unroll
-  for (int f = 0; f < 2; ++f) pf[f] = pair_flux(own[f], nb[f], P.gas.cg);
-  Real dd[2][5];
+  for (int f = 0; f < F; ++f) pf[f] = pair_flux(own[f], nb[f], P.gas.cg);
+  Real dd[F][5];
 #pragma unroll
-  for (int f = 0; f < 2; ++f)
+  for (int f = 0; f < F; ++f)
 #pragma unroll
     for (int v = 0; v < 5; ++v) dd[f][v] = Real(0);
   if (P.dissipation) {
 #pragma unroll
-    for (int f = 0; f < 2; ++f)
+    for (int f = 0; f < F; ++f)
       matrix_dissipation(own[f], nb[f], pf[f].rho_log, pf[f].inv_blog, P.gas, dd[f]);
   }
   const Real lift = P.lift[dir];
 #pragma unroll
-  for (int f = 0; f < 2; ++f) {
+  for (int f = 0; f < F; ++f) {
     Real fo[5];
     point_flux(own[f], P.gas.cg, fo);
     // commit_face_side (kernels.hpp:391-430)
-    const Real n_own = f ? Real(1) : Real(-1);
+    const Real n_own = (side0 + f) ? Real(1) : Real(-1);
     const Real g_own = pf[f].tg * own[f].hib;
     const Real phi_own = own[f].hphi + own[f].hphi;
     Real fl[5];
@@ -347,7 +369,8 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // Neighbour state of face lf, fetched one face ahead of its use so the
   // (mostly L2-resident) gather hides behind arithmetic. The six neighbour
   // codes were read at kernel start, so a fetch is one round trip, not two.
-  NbrRaw<Real> cur[2];
+  constexpr int FPI = VOL ? 2 : 1;
+  NbrRaw<Real> cur[FPI]; // the gathered neighbour trace(s) of the next face iteration
   auto fetch = [&](int lf, NbrRaw<Real>& r) {
     const int dir = lf >> 1, side = lf & 1;
     const int d1 = dir == 2 ? 0 : dir + 1;
@@ -441,7 +464,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   if (active) {
     if (SURF && !VOL) { // surface-only kernel: registers to spare, fetch early
       fetch(0, cur[0]);
-      fetch(1, cur[1]);
+      if (FPI == 2) fetch(1, cur[FPI - 1]);
     }
     // The NQ nodes are independent and computed stage by stage so that their
     // reciprocal and logarithm chains interleave. A non-physical node is
@@ -460,7 +483,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
       // logarithms (26 registers the fused kernel's node loop cannot spare);
       // they land while the CTA gathers at the barrier
       fetch(0, cur[0]);
-      fetch(1, cur[1]);
+      if (FPI == 2) fetch(1, cur[FPI - 1]);
     }
     if (bad >= 0) {
       const Real* qb = qe + bad * N2;
@@ -480,34 +503,42 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // by the z-line owners in phase A). Faces of one direction share no node,
   // faces of different directions do (edges), hence the two barriers.
   if (SURF) {
+    // FPI faces per iteration: 2 = both faces of a direction as two
+    // interleaved streams (measured best inside the fused kernels), 1 = one
+    // face at a time (half the code per iteration; measured best for the
+    // surface-only kernel: 5.45 vs 5.65 ms at configs[1])
 #pragma unroll 1
-    for (int dir = 0; dir < 3; ++dir) {
+    for (int lf = 0; lf < 6; lf += FPI) {
+      const int dir = lf >> 1, side0 = lf & 1;
       if (active) {
         const int d1 = dir == 2 ? 0 : dir + 1;
         const int d2 = d1 == 2 ? 0 : d1 + 1;
-        // node values of the two neighbour traces, then -- the raw traces are
-        // dead -- the next direction's gather into the same registers; it
-        // lands while this direction's fluxes are evaluated
-        Node<Real> nb[2];
-        face_pair_neighbours<Real, NQ>(P, cur, dir, eg, l, logtab, nb);
-        if (dir < 2) {
-          fetch(2 * dir + 2, cur[0]);
-          fetch(2 * dir + 3, cur[1]);
+        // node values of the neighbour traces, then -- the raw traces are
+        // dead -- the next gather into the same registers; it lands while
+        // this iteration's fluxes are evaluated
+        Node<Real> nb[FPI];
+        face_pair_neighbours<Real, NQ, FPI>(P, cur, dir, eg, l, logtab, nb);
+        if (lf + FPI < 6) {
+#pragma unroll
+          for (int f = 0; f < FPI; ++f) fetch(lf + FPI + f, cur[f]);
         }
         // FaceIndexer::node (mesh.hpp:107-114): tangential axes d1, d2
         const int s0 = e * N3P + l0 * spitch(d1) + l1 * spitch(d2);
-        const int s_own[2] = {s0, s0 + (NQ - 1) * spitch(dir)};
-        Node<Real> own[2];
-        own[0] = load_node(vals, VS, s_own[0], dir);
-        own[1] = load_node(vals, VS, s_own[1], dir);
-        Real c[2][5], o[2][5];
-        face_pair_contribution<Real, NQ>(P, own, nb, dir, c);
+        int s_own[FPI];
+        Node<Real> own[FPI];
+#pragma unroll
+        for (int f = 0; f < FPI; ++f) {
+          s_own[f] = s0 + ((side0 + f) ? (NQ - 1) * spitch(dir) : 0);
+          own[f] = load_node(vals, VS, s_own[f], dir);
+        }
+        Real c[FPI][5], o[FPI][5];
+        face_pair_contribution<Real, NQ, FPI>(P, own, nb, dir, side0, c);
         Real* tn = tend + (1 + dir) * VS;
         Real* tt1 = tend + (1 + d1) * VS;
         Real* tt2 = tend + (1 + d2) * VS;
         Real* t4 = tend + 4 * VS;
 #pragma unroll
-        for (int f = 0; f < 2; ++f) {
+        for (int f = 0; f < FPI; ++f) {
           o[f][0] = tend[s_own[f]];
           o[f][1] = tn[s_own[f]];
           o[f][2] = tt1[s_own[f]];
@@ -515,7 +546,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           o[f][4] = t4[s_own[f]];
         }
 #pragma unroll
-        for (int f = 0; f < 2; ++f) {
+        for (int f = 0; f < FPI; ++f) {
           tend[s_own[f]] = fma_(-P.gain, c[f][0], o[f][0]);
           tn[s_own[f]] = fma_(-P.gain, c[f][1], o[f][1]);
           tt1[s_own[f]] = fma_(-P.gain, c[f][2], o[f][2]);
@@ -523,7 +554,8 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           t4[s_own[f]] = fma_(-P.gain, c[f][4], o[f][4]);
         }
       }
-      __syncthreads();
+      // faces of one direction share no node, faces of different directions do
+      if (((lf + FPI) & 1) == 0) __syncthreads();
     }
   }
 
