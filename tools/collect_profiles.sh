@@ -11,6 +11,10 @@ timeout 300 python bench.py --path split --no-cpu-baseline > $OUT/${TAG}_bench_s
 timeout 300 python bench.py --path fused --no-cpu-baseline --no-e2e > $OUT/${TAG}_bench_fused.json 2> $OUT/${TAG}_bench_fused.err
 timeout 300 python bench.py --precision f32 --no-cpu-baseline > $OUT/${TAG}_bench_stage_f32.json 2> $OUT/${TAG}_bench_f32.err
 timeout 300 python bench.py --impl reference --steps 5 --warmup 1 > $OUT/${TAG}_bench_reference.json 2> $OUT/${TAG}_bench_reference.err
+timeout 300 python bench.py --case baroclinic --no-cpu-baseline > $OUT/${TAG}_bench_baroclinic.json 2> $OUT/${TAG}_bench_baroclinic.err
+timeout 600 python bench.py --case baroclinic --base 12 4 2 --steps 3 --no-cpu-baseline --no-e2e > $OUT/${TAG}_bench_baroclinic_4e8.json 2> $OUT/${TAG}_bench_baroclinic_4e8.err
+timeout 900 python tools/sweep_probe.py > $OUT/${TAG}_order_precision_sweep.jsonl 2> $OUT/${TAG}_sweep.err
+timeout 900 python tools/error_survey.py > $OUT/${TAG}_error_survey.txt 2>&1
 # every launch of the default bench command with its device time
 timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
   --log-file $OUT/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > $OUT/${TAG}_ncu_launches.log 2>&1
