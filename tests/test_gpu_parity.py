@@ -207,6 +207,33 @@ def test_trajectory_config1(port, path):
     assert abs(p_gpu - p_cpu) <= 1e-6 * abs(p_cpu) + 1e-9
 
 
+def test_entropy_evolution_config1(port):
+    """The total-entropy evolution agrees with the reference's (north star):
+    configs[0], stage path, device reductions, 40 LSRK steps. eta itself agrees
+    to rounding (it carries no signal beyond 15 digits); the
+    entropy production -- the signal -- to 1e-6 relative at every sample; mass
+    and energy do not drift. tools/entropy_evolution.py prints the long run
+    (profiles/r1_entropy_evolution.txt: 200 steps, 4e-8 relative)."""
+    o, g = make(port, "bubble", (3, False), 4, path=capi.PATH_STAGE)
+    g.set_state(o.init_case(po.CASE_BUBBLE_SHARP).copy())
+    dt = o.compute_dt(0.5)
+    m0, e0 = g.quadrature_total(0), g.quadrature_total(4)
+    for n in range(1, 41):
+        o.step(dt)
+        g.step(dt)
+        if n % 10:
+            continue
+        qs = o.state.copy()
+        eta_c, eta_g = o.total_entropy(qs), g.total_entropy()
+        assert abs(eta_g - eta_c) <= 1e-14 * abs(eta_c)
+        p_c = o.entropy_production(qs, o.assemble_rhs(qs))
+        g.rhs(0.0, 1.0)
+        p_g = g.entropy_production()
+        assert p_g < 0.0 and abs(p_g - p_c) <= 1e-6 * abs(p_c), (n, p_g, p_c)
+        assert abs(g.quadrature_total(0) - m0) <= 1e-14 * abs(m0)
+        assert abs(g.quadrature_total(4) - e0) <= 1e-14 * abs(e0)
+
+
 @pytest.mark.parametrize("path", [capi.PATH_SPLIT, capi.PATH_FUSED])
 @pytest.mark.parametrize("order,case,seed", [(4, po.CASE_ENTROPY_TEST, 20240501), (2, po.CASE_ENTROPY_TEST, 3),
                                              (7, po.CASE_ENTROPY_TEST, 4), (4, po.CASE_BUBBLE_SMOOTH, 0)])
