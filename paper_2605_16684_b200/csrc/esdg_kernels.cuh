@@ -33,6 +33,8 @@
 //   - commit: slab + registers -> out, coalesced over l.
 #pragma once
 
+#include <cstdio>
+
 #include "esdg_device.cuh"
 
 namespace esdg_b200 {
@@ -345,6 +347,14 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
 
   const int tid = threadIdx.x;
   const long long e0 = static_cast<long long>(blockIdx.x) * EPB;
+#ifdef ESDG_TUNE_PHASE_CLOCKS
+  long long tclk[10];
+  int nclk = 0;
+#define ESDG_CLK() tclk[nclk++] = clock64()
+#else
+#define ESDG_CLK()
+#endif
+  ESDG_CLK();
 
   // thread <-> (element e, line l = l0 + NQ l1). In phase A, in the z sweep
   // and in the commit the thread owns the z line through (x, y) = (l0, l1),
@@ -460,7 +470,9 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // the logarithm's table (FP64): fetched behind the state loads, visible to
   // the CTA before the first logarithm
   store_log_table(logtab, ltab, tid, EPB * N2);
+  ESDG_CLK();
   if (sizeof(Real) == 8) __syncthreads();
+  ESDG_CLK();
   if (active) {
     if (SURF && !VOL) { // surface-only kernel: registers to spare, fetch early
       fetch(0, cur[0]);
@@ -495,8 +507,10 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
                  double(qq[0]), double(pr));
     }
   }
+  ESDG_CLK();
   cp_async_wait_all(); // this thread's share of out_old is in the slab
   __syncthreads();
+  ESDG_CLK();
 
   // ---- phase C: the six faces, thread per face node -----------------------
   // Every face subtracts its lift term from the shared tendency slab (zeroed
@@ -559,6 +573,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     }
   }
 
+  ESDG_CLK();
   // ---- phase B: the three line sweeps, one code instance -------------------
   // x and y results are handed to the z-line owners through the shared slab;
   // the z sweep stays in registers because the same thread commits that line.
@@ -631,6 +646,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     }
   }
 
+  ESDG_CLK();
   // ---- commit: slab (old out, faces, x, y) + registers (z) on the z line ----
   if (active) {
     // acc: rotated frame of z: normal -> var 3, t1 = x -> 1, t2 = y -> 2
@@ -705,6 +721,13 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           qn[v * N3 + k * N2] = qv[k][v] + P.b_upd * knew[k][v];
     }
   }
+#ifdef ESDG_TUNE_PHASE_CLOCKS
+  ESDG_CLK();
+  if (tid == 0 && blockIdx.x == 40000)
+    printf("phase clocks VOL=%d SURF=%d: loads %lld | table barrier %lld | nodes %lld | barrier %lld | faces %lld | sweeps %lld | commit %lld | total %lld\n",
+           int(VOL), int(SURF), tclk[1] - tclk[0], tclk[2] - tclk[1], tclk[3] - tclk[2], tclk[4] - tclk[3],
+           tclk[5] - tclk[4], tclk[6] - tclk[5], tclk[7] - tclk[6], tclk[7] - tclk[0]);
+#endif
 }
 
 // K3: q += b k (solver.hpp:342-353). Pure stream: 2 reads + 1 write per
