@@ -127,6 +127,32 @@ struct Geo {
   }
 };
 
+// Elements per CTA (EPB) and the resident-CTA target handed to
+// __launch_bounds__ (MINB): EPB*NQ^2 threads should fill whole warps, MINB
+// CTAs must fit an SM's 227 KB of shared memory at 14 quantity arrays per
+// node, and the register cap 65536/(MINB*threads) must not spill the line
+// state (ptxas -v is checked in DESIGN.md).
+template <int NQ, int BYTES>
+struct Tile;
+template <> struct Tile<2, 8> { static constexpr int EPB = 32, MINB = 4; static constexpr bool LEAN = false; };
+template <> struct Tile<3, 8> { static constexpr int EPB = 14, MINB = 4; static constexpr bool LEAN = false; };
+template <> struct Tile<4, 8> { static constexpr int EPB = 8, MINB = 3; static constexpr bool LEAN = false; };
+#ifndef ESDG_TUNE_EPB
+#define ESDG_TUNE_EPB 5
+#define ESDG_TUNE_MINB 3
+#endif
+template <> struct Tile<5, 8> { static constexpr int EPB = ESDG_TUNE_EPB, MINB = ESDG_TUNE_MINB; static constexpr bool LEAN = false; };
+template <> struct Tile<6, 8> { static constexpr int EPB = 3, MINB = 2; static constexpr bool LEAN = false; };
+template <> struct Tile<7, 8> { static constexpr int EPB = 2, MINB = 2; static constexpr bool LEAN = true; };
+template <> struct Tile<8, 8> { static constexpr int EPB = 1, MINB = 3; static constexpr bool LEAN = true; };
+template <> struct Tile<2, 4> { static constexpr int EPB = 32, MINB = 4; static constexpr bool LEAN = false; };
+template <> struct Tile<3, 4> { static constexpr int EPB = 14, MINB = 4; static constexpr bool LEAN = false; };
+template <> struct Tile<4, 4> { static constexpr int EPB = 8, MINB = 4; static constexpr bool LEAN = false; };
+template <> struct Tile<5, 4> { static constexpr int EPB = 5, MINB = 4; static constexpr bool LEAN = false; };
+template <> struct Tile<6, 4> { static constexpr int EPB = 3, MINB = 4; static constexpr bool LEAN = false; };
+template <> struct Tile<7, 4> { static constexpr int EPB = 2, MINB = 4; static constexpr bool LEAN = false; };
+template <> struct Tile<8, 4> { static constexpr int EPB = 2, MINB = 2; static constexpr bool LEAN = false; };
+
 template <class Real>
 __device__ __forceinline__ Node<Real> load_node(const Real* vals, int VS, int s,
                                                 int dir) {
@@ -177,9 +203,38 @@ template <class Real, int NQ>
 __device__ __forceinline__ void sweep_line(const RhsParams<Real, NQ>& P,
                                            const Real* vals, int VS, int base,
                                            int stride, int dir, Real (&acc)[NQ][5]) {
+  // At the highest orders a line's node values and accumulators (14 NQ
+  // Reals) no longer fit the register file next to the flux temporaries.
+  // There only the five quantities every pair uses twice stay resident;
+  // log rho/2, log b, phi/2 and 1/(2b) are fetched from shared memory for
+  // the pair at hand (the load/store pipe has room: 2 NQ (NQ-1) extra loads
+  // per line against 24 NQ (NQ-1) FP64 instructions).
+  constexpr bool kLean = Tile<NQ, sizeof(Real)>::LEAN;
   Node<Real> nd[NQ];
+  const int d1l = dir == 2 ? 0 : dir + 1;
+  const int d2l = d1l == 2 ? 0 : d1l + 1;
 #pragma unroll
-  for (int i = 0; i < NQ; ++i) nd[i] = load_node(vals, VS, base + i * stride, dir);
+  for (int i = 0; i < NQ; ++i) {
+    if (kLean) {
+      const int sn = base + i * stride;
+      nd[i].hr = vals[V_HR * VS + sn];
+      nd[i].hun = vals[(V_HU0 + dir) * VS + sn];
+      nd[i].hut1 = vals[(V_HU0 + d1l) * VS + sn];
+      nd[i].hut2 = vals[(V_HU0 + d2l) * VS + sn];
+      nd[i].b = vals[V_B * VS + sn];
+    } else {
+      nd[i] = load_node(vals, VS, base + i * stride, dir);
+    }
+  }
+  auto cold = [&](int i) {
+    if (kLean) {
+      const int sn = base + i * stride;
+      nd[i].hlr = vals[V_HLR * VS + sn];
+      nd[i].lb = vals[V_LB * VS + sn];
+      nd[i].hphi = vals[V_HPHI * VS + sn];
+      nd[i].hib = vals[V_HIB * VS + sn];
+    }
+  };
   // diagonal: t_i -= 2 g_d D_ii F(q_i, q_i)  (kernels.hpp:170-188). D_ii
   // vanishes analytically at interior LGL nodes; the host flushes its
   // O(1e-16) round-off residue to zero (shard.cu), so only the two end nodes
@@ -188,6 +243,7 @@ __device__ __forceinline__ void sweep_line(const RhsParams<Real, NQ>& P,
   for (int i = 0; i < NQ; i += NQ - 1) {
     const Real cii = P.negd[i * NQ + i];
     Real f[5];
+    cold(i);
     point_flux(nd[i], P.gas.cg, f);
 #pragma unroll
     for (int v = 0; v < 5; ++v) acc[i][v] = fma_(cii, f[v], acc[i][v]);
@@ -220,6 +276,8 @@ __device__ __forceinline__ void sweep_line(const RhsParams<Real, NQ>& P,
 #pragma unroll
     for (int j = 0; j < NQ; ++j) {
       if (j <= i) continue; // constant bounds keep the unroll total
+      cold(i);
+      cold(j);
       const PairFlux<Real> pf = pair_flux(nd[i], nd[j], P.gas.cg);
       const Real cij = P.negd[i * NQ + j];
       const Real cji = P.negd[j * NQ + i];
@@ -784,32 +842,6 @@ __global__ void __launch_bounds__(256)
     send[i] = q[(static_cast<long long>(send_elem[slot]) * 5 + v) * N3 + node];
   }
 }
-
-// Elements per CTA (EPB) and the resident-CTA target handed to
-// __launch_bounds__ (MINB): EPB*NQ^2 threads should fill whole warps, MINB
-// CTAs must fit an SM's 227 KB of shared memory at 14 quantity arrays per
-// node, and the register cap 65536/(MINB*threads) must not spill the line
-// state (ptxas -v is checked in DESIGN.md).
-template <int NQ, int BYTES>
-struct Tile;
-template <> struct Tile<2, 8> { static constexpr int EPB = 32, MINB = 4; };
-template <> struct Tile<3, 8> { static constexpr int EPB = 14, MINB = 4; };
-template <> struct Tile<4, 8> { static constexpr int EPB = 8, MINB = 3; };
-#ifndef ESDG_TUNE_EPB
-#define ESDG_TUNE_EPB 5
-#define ESDG_TUNE_MINB 3
-#endif
-template <> struct Tile<5, 8> { static constexpr int EPB = ESDG_TUNE_EPB, MINB = ESDG_TUNE_MINB; };
-template <> struct Tile<6, 8> { static constexpr int EPB = 3, MINB = 2; };
-template <> struct Tile<7, 8> { static constexpr int EPB = 2, MINB = 2; };
-template <> struct Tile<8, 8> { static constexpr int EPB = 1, MINB = 3; };
-template <> struct Tile<2, 4> { static constexpr int EPB = 32, MINB = 4; };
-template <> struct Tile<3, 4> { static constexpr int EPB = 14, MINB = 4; };
-template <> struct Tile<4, 4> { static constexpr int EPB = 8, MINB = 4; };
-template <> struct Tile<5, 4> { static constexpr int EPB = 5, MINB = 4; };
-template <> struct Tile<6, 4> { static constexpr int EPB = 3, MINB = 4; };
-template <> struct Tile<7, 4> { static constexpr int EPB = 2, MINB = 4; };
-template <> struct Tile<8, 4> { static constexpr int EPB = 2, MINB = 2; };
 
 } // namespace dev
 } // namespace esdg_b200
