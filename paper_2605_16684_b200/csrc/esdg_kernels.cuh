@@ -13,24 +13,36 @@
 // Execution model of rhs_kernel (B200: 148 SMs, 64 FP64 lanes/SM, 227 KB smem)
 //   - one CTA owns EPB consecutive (Morton) elements; EPB*NQ^2 threads; thread
 //     (e, l) is "line l of element e" throughout.
-//   - phase A: the thread loads the NQ nodes of its z line straight from HBM
-//     (coalesced over l), computes primitives + both logarithms once per node
-//     (precompute/logmean rungs of the reference's ladder) and parks them in
-//     shared memory, SoA per quantity.
-//   - phase B, thread per node LINE: the thread pulls its line's NQ nodes
-//     into registers and evaluates every unordered pair (i,j) exactly once,
-//     adding c_ij (S + G e_n) to node i and c_ji (S - G b_i/b_j e_n) to node
-//     j in registers (the paper's pair symmetry incl. the -G b-/b+ rule for
-//     the non-symmetric gravity term). No partner exchange is needed, so the
-//     shared-memory pipe only sees the line load and the tendency update.
-//     x and y sweeps go through the shared tendency slab; the z sweep stays
-//     in registers because the same thread commits that z line.
-//   - phase C, thread per face node: each element side evaluates the
-//     canonical (minus,plus) flux of its own face -- the flux is a pure
-//     function of the two traces, so both sides obtain bitwise identical
-//     values and conservation is exact without storing face records. x and y
-//     faces update the shared slab, z faces the thread's own registers.
-//   - commit: slab + registers -> out, coalesced over l.
+//   - phase A: every global load is issued first -- the NQ nodes of the
+//     thread's z line (coalesced over l), the logarithm table, L2 prefetches
+//     for the next resident wave and, in the accumulate form, cp.async copies
+//     of the old `out` into the shared tendency slab. Then primitives and both
+//     logarithms once per node (precompute/logmean rungs of the reference's
+//     ladder), the NQ nodes stage by stage, parked in shared memory, SoA per
+//     quantity.
+//   - the slab holds T = out_old + gain * (contributions), gain = a_new/a_old;
+//     every later phase adds its share with one FMA, the commit writes
+//     a_old * T (a_old == 0: a_new * contributions, `out` is never read).
+//   - phase C (SURF), thread per face node, runs before the sweeps: each
+//     element side evaluates the canonical (minus,plus) flux of its own face
+//     -- the flux is a pure function of the two traces, so both sides obtain
+//     bitwise identical values and conservation is exact without storing
+//     face records. All six faces update the slab; a reflecting wall is the
+//     element's own trace with the normal momentum negated.
+//   - phase B (VOL), thread per node LINE: the thread pulls its line's NQ
+//     nodes into registers and evaluates every unordered pair (i,j) exactly
+//     once, adding c_ij (S + G e_n) to node i and c_ji (S - G b_i/b_j e_n) to
+//     node j in registers (the paper's pair symmetry incl. the -G b-/b+ rule
+//     for the non-symmetric gravity term). No partner exchange is needed, so
+//     the shared-memory pipe only sees the line load and the slab update.
+//     The coefficients -(2 D_ij) are direction independent (uniform
+//     registers); the metric is applied when the sums are handed on. x and y
+//     sweeps go through the slab; the z sweep stays in registers because the
+//     same thread commits that z line.
+//   - commit: slab + registers -> out (+ Coriolis, + the fused LSRK register
+//     update), coalesced over l, no global load to wait for except the state
+//     re-read of the fused update.
+// DESIGN.md section 4 has the measurements behind these choices.
 #pragma once
 
 #include <cstdio>
