@@ -469,6 +469,10 @@ private:
     // slab arithmetic of rhs_kernel: T = out_old + gain * rhs, out = fin * T
     P.gain = P.a_old != Real(0) ? P.a_new / P.a_old : P.a_new;
     P.fin = P.a_old != Real(0) ? P.a_old : Real(1);
+    if (!std::isfinite(double(P.gain))) {
+      set_message("rhs: a_new / a_old is not finite (pass a_old = 0 to overwrite out)");
+      return cudaErrorInvalidValue;
+    }
     P.gas = gas_;
     for (int i = 0; i < NQ * NQ; ++i) P.negd[i] = negd_[size_t(i)];
     for (int k = 0; k < 3; ++k) {

@@ -393,3 +393,24 @@ def test_axpy_and_lsrk_pieces(port):
     g.set_state(k, capi.REG_K)
     g.axpy(0.37)
     assert np.array_equal(g.get_state(), q + 0.37 * k)
+
+
+def test_runner_outputs(tmp_path):
+    """run_case on the GPU solver writes the reference runner's files and
+    columns (runner.cpp:205-267); the bubble conserves mass and energy and
+    dissipates entropy."""
+    from paper_2605_16684_b200 import runner
+    res = runner.run_case("bubble", order=3, refinement=2, steps=12, output_cadence=4,
+                          out_dir=str(tmp_path), path=capi.PATH_STAGE)
+    assert res["status"] == "ok" and res["steps"] == 12
+    heads = {"conservation.csv": "step,time,mass,energy,mass_drift,energy_drift",
+             "entropy.csv": "step,time,total_entropy,entropy_production",
+             "throughput.csv": "elements,steps,wall_time_s,element_steps_per_s",
+             "roofline.csv": "kernel,ai,gflops,fraction_of_roof"}
+    for name, head in heads.items():
+        lines = (tmp_path / name).read_text().strip().splitlines()
+        assert lines[0] == head and len(lines) >= 2, name
+    assert len((tmp_path / "conservation.csv").read_text().strip().splitlines()) == 1 + 4
+    assert res["mass_drift"] <= 1e-14 and res["energy_drift"] <= 1e-14
+    assert all(row[3] <= 0.0 for row in res["entropy"])
+    assert "# status = ok" in (tmp_path / "manifest.txt").read_text()
