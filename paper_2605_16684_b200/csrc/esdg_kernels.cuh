@@ -518,23 +518,24 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
 #pragma unroll
         for (int v = 0; v < 5; ++v) tend[v * VS + zbase + k * ZS] = Real(0);
     }
-    // the q / phi / out slabs of the CTA that will follow this one on the SM
-    // (one resident wave ahead), so its phase A starts from L2, not HBM
-    {
-      const long long en = e0 + static_cast<long long>(P.prefetch_ctas) * EPB;
-      if (en + EPB <= P.ne) {
-        const char* qb = reinterpret_cast<const char*>(P.q + en * (5 * N3));
-        for (int off = tid * 128; off < EPB * 5 * N3 * int(sizeof(Real)); off += EPB * N2 * 128)
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(qb + off));
-        const char* pb = reinterpret_cast<const char*>(P.phi + en * N3);
-        for (int off = tid * 128; off < EPB * N3 * int(sizeof(Real)); off += EPB * N2 * 128)
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + off));
-        if (read_out) {
-          const char* ob = reinterpret_cast<const char*>(P.out + en * (5 * N3));
-          for (int off = tid * 128; off < EPB * 5 * N3 * int(sizeof(Real)); off += EPB * N2 * 128)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(ob + off));
-        }
-      }
+  }
+  // the q / phi / out slabs of the CTA that will follow this one on the SM
+  // (one resident wave ahead), so its phase A starts from L2, not HBM: three
+  // bulk prefetches (TMA engine, no registers, no load/store-pipe traffic)
+  // instead of one prefetch instruction per 128 bytes -- those brought in
+  // single sectors, and a quarter of the demand loads still missed L2
+  {
+    const long long en = e0 + static_cast<long long>(P.prefetch_ctas) * EPB;
+    if (tid < 3 && en + EPB <= P.ne && (tid < 2 || read_out)) {
+      const char* base = tid == 0   ? reinterpret_cast<const char*>(P.q + en * (5 * N3))
+                         : tid == 1 ? reinterpret_cast<const char*>(P.phi + en * N3)
+                                    : reinterpret_cast<const char*>(P.out + en * (5 * N3));
+      const unsigned bytes = (tid == 1 ? EPB * N3 : EPB * 5 * N3) * unsigned(sizeof(Real));
+      // 16-byte aligned start and size that cover [base, base + bytes)
+      const unsigned long long lo = reinterpret_cast<unsigned long long>(base) & ~15ull;
+      const unsigned long long hi = (reinterpret_cast<unsigned long long>(base) + bytes + 15ull) & ~15ull;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(unsigned(hi - lo))
+                   : "memory");
     }
   }
   // the logarithm's table (FP64): fetched behind the state loads, visible to
