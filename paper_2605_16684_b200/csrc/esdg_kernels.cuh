@@ -211,7 +211,7 @@ __device__ __forceinline__ Node<Real> rotate_node(const Real nv[V_COUNT],
 // FP64 pipe for three cycles instead of two). One code instance
 // serves the three directions (the instruction cache is a real constraint
 // for these fully unrolled bodies).
-template <class Real, int NQ>
+template <class Real, int NQ, bool DIAG>
 __device__ __forceinline__ void sweep_line(const RhsParams<Real, NQ>& P,
                                            const Real* vals, int VS, int base,
                                            int stride, int dir, Real (&acc)[NQ][5]) {
@@ -251,14 +251,23 @@ __device__ __forceinline__ void sweep_line(const RhsParams<Real, NQ>& P,
   // vanishes analytically at interior LGL nodes; the host flushes its
   // O(1e-16) round-off residue to zero (shard.cu), so only the two end nodes
   // carry a point flux -- known at compile time, no branch.
+  // In the fused kernels even those two are skipped together with the
+  // -n F(q_own) part of the surface term: -2 g_d D_00 = g_d / w_0 = lift_d
+  // (and +lift_d at the other end) by the SBP property of the LGL operator,
+  // so the two point-flux terms of an end node cancel analytically. The
+  // reference evaluates both and lets them cancel to rounding
+  // (kernels.hpp:170-188, 406-428); dropping the pair changes a tendency by
+  // 1e-16 of the flux and saves 2 x 6 NQ^2 point fluxes per element.
+  if (DIAG) {
 #pragma unroll
-  for (int i = 0; i < NQ; i += NQ - 1) {
-    const Real cii = P.negd[i * NQ + i];
-    Real f[5];
-    cold(i);
-    point_flux(nd[i], P.gas.cg, f);
+    for (int i = 0; i < NQ; i += NQ - 1) {
+      const Real cii = P.negd[i * NQ + i];
+      Real f[5];
+      cold(i);
+      point_flux(nd[i], P.gas.cg, f);
 #pragma unroll
-    for (int v = 0; v < 5; ++v) acc[i][v] = fma_(cii, f[v], acc[i][v]);
+      for (int v = 0; v < 5; ++v) acc[i][v] = fma_(cii, f[v], acc[i][v]);
+    }
   }
 #ifdef ESDG_LADDER_NO_SYMMETRY
   // Ladder rung without pair symmetry (the reference's "logmean" variant,
@@ -364,7 +373,7 @@ __device__ __forceinline__ void face_pair_neighbours(const RhsParams<Real, NQ>& 
 }
 
 // Part 2: fluxes, dissipation and lift of the two faces.
-template <class Real, int NQ, int F>
+template <class Real, int NQ, int F, bool OWN>
 __device__ __forceinline__ void face_pair_contribution(const RhsParams<Real, NQ>& P,
                                                        const Node<Real> (&own)[F],
                                                        const Node<Real> (&nb)[F], int dir,
@@ -385,9 +394,11 @@ __device__ __forceinline__ void face_pair_contribution(const RhsParams<Real, NQ>
   const Real lift = P.lift[dir];
 #pragma unroll
   for (int f = 0; f < F; ++f) {
-    Real fo[5];
-    point_flux(own[f], P.gas.cg, fo);
-    // commit_face_side (kernels.hpp:391-430)
+    // commit_face_side (kernels.hpp:391-430); OWN = false in the fused
+    // kernels: -n F(q_own) cancels against the volume term's diagonal, see
+    // sweep_line
+    Real fo[5] = {Real(0), Real(0), Real(0), Real(0), Real(0)};
+    if (OWN) point_flux(own[f], P.gas.cg, fo);
     const Real n_own = (side0 + f) ? Real(1) : Real(-1);
     const Real g_own = pf[f].tg * own[f].hib;
     const Real phi_own = own[f].hphi + own[f].hphi;
@@ -398,7 +409,7 @@ __device__ __forceinline__ void face_pair_contribution(const RhsParams<Real, NQ>
     fl[3] = n_own * pf[f].f[3] - Real(0.5) * dd[f][3];
     fl[4] = n_own * pf[f].f[4] - Real(0.5) * fma_(phi_own, dd[f][0], dd[f][4]);
 #pragma unroll
-    for (int v = 0; v < 5; ++v) c[f][v] = lift * (fl[v] - n_own * fo[v]);
+    for (int v = 0; v < 5; ++v) c[f][v] = OWN ? lift * (fl[v] - n_own * fo[v]) : lift * fl[v];
   }
 }
 
@@ -617,7 +628,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           own[f] = load_node(vals, VS, s_own[f], dir);
         }
         Real c[FPI][5], o[FPI][5];
-        face_pair_contribution<Real, NQ, FPI>(P, own, nb, dir, side0, c);
+        face_pair_contribution<Real, NQ, FPI, !(VOL && SURF)>(P, own, nb, dir, side0, c);
         Real* tn = tend + (1 + dir) * VS;
         Real* tt1 = tend + (1 + d1) * VS;
         Real* tt2 = tend + (1 + d2) * VS;
@@ -668,7 +679,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         for (int i = 0; i < NQ; ++i)
 #pragma unroll
           for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
-        sweep_line<Real, NQ>(P, vals, VS, base, stride, dir, acc);
+        sweep_line<Real, NQ, !(VOL && SURF)>(P, vals, VS, base, stride, dir, acc);
         if (dir < 2) {
           // un-rotate into the slab: normal -> 1+dir, then cyclic. Without
           // faces the x sweep is the slab's first writer and simply stores;
