@@ -15,9 +15,7 @@ cudaError_t launch_one(const dev::RhsParams<Real, NQ>& P, cudaStream_t stream) {
 #ifndef ESDG_TUNE_EXTRA_SMEM
 #define ESDG_TUNE_EXTRA_SMEM 0
 #endif
-  constexpr size_t smem =
-      (size_t(dev::V_COUNT + 5) * EPB * dev::Geo<NQ>::N3P + dev::LogTab<Real>::kReals) *
-          sizeof(Real) + ESDG_TUNE_EXTRA_SMEM;
+  constexpr size_t smem = dev::SmemMap<Real, NQ, EPB>::kBytes + ESDG_TUNE_EXTRA_SMEM;
   auto kern = dev::rhs_kernel<Real, NQ, EPB, MINB, VOL, SURF>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -62,8 +60,7 @@ void rhs_launch_shape(int* threads, int* epb, size_t* smem_bytes) {
   constexpr int EPB = dev::Tile<NQ, sizeof(Real)>::EPB;
   *threads = EPB * NQ * NQ;
   *epb = EPB;
-  *smem_bytes = (size_t(dev::V_COUNT + 5) * EPB * dev::Geo<NQ>::N3P +
-                 dev::LogTab<Real>::kReals) * sizeof(Real);
+  *smem_bytes = dev::SmemMap<Real, NQ, EPB>::kBytes;
 }
 
 #define ESDG_INSTANTIATE(REAL, NQ)                                             \

@@ -127,6 +127,39 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
+// TMA bulk copy global -> shared completing on an mbarrier (sm_90+): one
+// instruction moves a whole contiguous slab without registers, L1 or the
+// load/store pipe. Source, destination and size must be multiples of 16 B.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@p bra DONE_%=;\n\tbra WAIT_%=;\n\tDONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 template <int NQ>
 struct Geo {
   static constexpr int N2 = NQ * NQ;
@@ -138,6 +171,30 @@ struct Geo {
     return (n - bc * NQ) + PX * bc;
   }
 };
+
+// Shared-memory map of rhs_kernel (bytes). With an unpadded node layout (odd
+// NQ) the element slabs of q, phi and out are contiguous in HBM exactly as
+// the kernel wants them in shared memory, so they arrive by TMA bulk copies:
+// q and phi into the (still unused) front of the node-value arrays, out into
+// the tendency slab, which then uses the [element][variable][node] order of
+// the state registers. A slab starts at a multiple of sizeof(Real), not of
+// 16 B, in HBM: the copy starts up to 12 B early and the data sit at the same
+// offset in shared memory, hence the slack words.
+template <class Real, int NQ, int EPB>
+struct SmemMap {
+  using G = Geo<NQ>;
+  static constexpr bool kBulk = G::PX == NQ;
+  static constexpr int VS = EPB * G::N3P;
+  static constexpr size_t up16(size_t x) { return (x + 15) & ~size_t(15); }
+  static constexpr size_t kStagePhi = up16(size_t(EPB) * 5 * G::N3 * sizeof(Real) + 16);
+  static constexpr size_t kTend = up16(size_t(V_COUNT) * VS * sizeof(Real));
+  static constexpr size_t kTab = kTend + up16((size_t(5) * VS + 4) * sizeof(Real));
+  static constexpr size_t kBar = kTab + up16(size_t(LogTab<Real>::kReals) * sizeof(Real));
+  static constexpr size_t kBytes = kBar + 16;
+  static_assert(!kBulk || kStagePhi + up16(size_t(EPB) * G::N3 * sizeof(Real) + 16) <= kTend,
+                "q and phi staging must fit in front of the slab");
+};
+
 
 // Elements per CTA (EPB) and the resident-CTA target handed to
 // __launch_bounds__ (MINB): EPB*NQ^2 threads should fill whole warps, MINB
@@ -421,10 +478,12 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   constexpr int VS = EPB * N3P; // stride between quantity arrays
   constexpr int ZS = PX * NQ;   // shared-memory pitch of the z axis
 
+  using Map = SmemMap<Real, NQ, EPB>;
+  constexpr bool kBulk = Map::kBulk;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Real* vals = reinterpret_cast<Real*>(smem_raw); // [V_COUNT][VS]
-  Real* tend = vals + V_COUNT * VS;               // [5][VS]
-  Real* logtab = tend + 5 * VS;                   // FP64 only: logarithm table
+  Real* vals = reinterpret_cast<Real*>(smem_raw);             // [V_COUNT][VS]
+  Real* logtab = reinterpret_cast<Real*>(smem_raw + Map::kTab); // FP64 only: logarithm table
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(smem_raw + Map::kBar);
 
   const int tid = threadIdx.x;
   const long long e0 = static_cast<long long>(blockIdx.x) * EPB;
@@ -446,6 +505,17 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   const bool active = eg < P.ne; // only the last CTA has idle lines
   const int zbase = e * N3P + l0 + PX * l1;
   const bool read_out = !VOL || P.a_old != Real(0);
+  // The tendency slab as this thread addresses it: variable v of shared index
+  // s (which includes the element offset e * N3P) is tslab[v * TV + s]. TMA
+  // layout: [element][variable][node] shifted by the source's misalignment;
+  // otherwise [variable][element][node].
+  const long long slab0 = e0 * (5 * N3);
+  const unsigned off_q = unsigned(reinterpret_cast<unsigned long long>(P.q + slab0) & 15u);
+  const unsigned off_p = unsigned(reinterpret_cast<unsigned long long>(P.phi + e0 * N3) & 15u);
+  const unsigned off_o = unsigned(reinterpret_cast<unsigned long long>(P.out + slab0) & 15u);
+  constexpr int TV = kBulk ? N3P : VS;
+  Real* tslab = kBulk ? reinterpret_cast<Real*>(smem_raw + Map::kTend + off_o) + 4 * e * N3P
+                      : reinterpret_cast<Real*>(smem_raw + Map::kTend);
 
   // pitches of the three axes in shared (padded) and global node numbering
   auto spitch = [](int ax) { return ax == 0 ? 1 : (ax == 1 ? PX : PX * NQ); };
@@ -507,27 +577,57 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   const Real* pe = P.phi + eg * N3 + l;
   Real qv[NQ][5], ph[NQ], ltab[kLogTabRegs];
   static_assert(EPB * N2 * kLogTabRegs >= LogTab<Real>::kReals, "CTA too small for the table");
-  load_log_table(ltab, tid, EPB * N2);
-  if (active) {
-#pragma unroll
-    for (int k = 0; k < NQ; ++k) {
-#pragma unroll
-      for (int v = 0; v < 5; ++v) qv[k][v] = qe[v * N3 + k * N2];
-      ph[k] = pe[k * N2];
+  if (kBulk) {
+    // One thread moves the CTA's slabs of q, phi and (accumulate form) out
+    // with three TMA bulk copies; everybody else only waits on the mbarrier.
+    if (tid == 0) mbar_init(mbar, 1);
+    __syncthreads();
+    if (tid == 0) {
+      const long long left = P.ne - e0;
+      const unsigned nel = left < EPB ? unsigned(left) : unsigned(EPB);
+      const unsigned bq = (off_q + nel * 5 * N3 * unsigned(sizeof(Real)) + 15u) & ~15u;
+      const unsigned bp = (off_p + nel * N3 * unsigned(sizeof(Real)) + 15u) & ~15u;
+      const unsigned bo =
+          read_out ? (off_o + nel * 5 * N3 * unsigned(sizeof(Real)) + 15u) & ~15u : 0u;
+      mbar_expect_tx(mbar, bq + bp + bo);
+      bulk_g2s(smem_raw, reinterpret_cast<const char*>(P.q + slab0) - off_q, bq, mbar);
+      bulk_g2s(smem_raw + Map::kStagePhi, reinterpret_cast<const char*>(P.phi + e0 * N3) - off_p, bp,
+               mbar);
+      if (read_out)
+        bulk_g2s(smem_raw + Map::kTend, reinterpret_cast<const char*>(P.out + slab0) - off_o, bo,
+                 mbar);
     }
-    if (read_out) {
-      const Real* oe = P.out + eg * (5 * N3) + l;
-#pragma unroll
-      for (int k = 0; k < NQ; ++k)
-#pragma unroll
-        for (int v = 0; v < 5; ++v)
-          cp_async<sizeof(Real)>(&tend[v * VS + zbase + k * ZS], oe + v * N3 + k * N2);
-    } else if (SURF) {
+    load_log_table(ltab, tid, EPB * N2);
+    if (!read_out && SURF && active) {
       // the faces are the slab's first writers and touch surface nodes only
 #pragma unroll
       for (int k = 0; k < NQ; ++k)
 #pragma unroll
-        for (int v = 0; v < 5; ++v) tend[v * VS + zbase + k * ZS] = Real(0);
+        for (int v = 0; v < 5; ++v) tslab[v * TV + zbase + k * ZS] = Real(0);
+    }
+  } else {
+    load_log_table(ltab, tid, EPB * N2);
+    if (active) {
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) {
+#pragma unroll
+        for (int v = 0; v < 5; ++v) qv[k][v] = qe[v * N3 + k * N2];
+        ph[k] = pe[k * N2];
+      }
+      if (read_out) {
+        const Real* oe = P.out + eg * (5 * N3) + l;
+#pragma unroll
+        for (int k = 0; k < NQ; ++k)
+#pragma unroll
+          for (int v = 0; v < 5; ++v)
+            cp_async<sizeof(Real)>(&tslab[v * TV + zbase + k * ZS], oe + v * N3 + k * N2);
+      } else if (SURF) {
+        // the faces are the slab's first writers and touch surface nodes only
+#pragma unroll
+        for (int k = 0; k < NQ; ++k)
+#pragma unroll
+          for (int v = 0; v < 5; ++v) tslab[v * TV + zbase + k * ZS] = Real(0);
+      }
     }
   }
   // the q / phi / out slabs of the CTA that will follow this one on the SM
@@ -552,8 +652,23 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // the logarithm's table (FP64): fetched behind the state loads, visible to
   // the CTA before the first logarithm
   store_log_table(logtab, ltab, tid, EPB * N2);
+  if (kBulk) {
+    // the slabs have landed: every thread takes the raw values of its z line
+    // out of the staging area, which the node values are about to overwrite
+    mbar_wait(mbar, 0);
+    if (active) {
+      const Real* sq = reinterpret_cast<const Real*>(smem_raw + off_q) + e * (5 * N3) + l;
+      const Real* sp = reinterpret_cast<const Real*>(smem_raw + Map::kStagePhi + off_p) + e * N3 + l;
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) {
+#pragma unroll
+        for (int v = 0; v < 5; ++v) qv[k][v] = sq[v * N3 + k * N2];
+        ph[k] = sp[k * N2];
+      }
+    }
+  }
   ESDG_CLK();
-  if (sizeof(Real) == 8) __syncthreads();
+  if (sizeof(Real) == 8 || kBulk) __syncthreads();
   ESDG_CLK();
   if (active) {
     if (SURF && !VOL) { // surface-only kernel: registers to spare, fetch early
@@ -629,13 +744,13 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         }
         Real c[FPI][5], o[FPI][5];
         face_pair_contribution<Real, NQ, FPI, !(VOL && SURF)>(P, own, nb, dir, side0, c);
-        Real* tn = tend + (1 + dir) * VS;
-        Real* tt1 = tend + (1 + d1) * VS;
-        Real* tt2 = tend + (1 + d2) * VS;
-        Real* t4 = tend + 4 * VS;
+        Real* tn = tslab + (1 + dir) * TV;
+        Real* tt1 = tslab + (1 + d1) * TV;
+        Real* tt2 = tslab + (1 + d2) * TV;
+        Real* t4 = tslab + 4 * TV;
 #pragma unroll
         for (int f = 0; f < FPI; ++f) {
-          o[f][0] = tend[s_own[f]];
+          o[f][0] = tslab[s_own[f]];
           o[f][1] = tn[s_own[f]];
           o[f][2] = tt1[s_own[f]];
           o[f][3] = tt2[s_own[f]];
@@ -643,7 +758,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         }
 #pragma unroll
         for (int f = 0; f < FPI; ++f) {
-          tend[s_own[f]] = fma_(-P.gain, c[f][0], o[f][0]);
+          tslab[s_own[f]] = fma_(-P.gain, c[f][0], o[f][0]);
           tn[s_own[f]] = fma_(-P.gain, c[f][1], o[f][1]);
           tt1[s_own[f]] = fma_(-P.gain, c[f][2], o[f][2]);
           tt2[s_own[f]] = fma_(-P.gain, c[f][3], o[f][3]);
@@ -687,17 +802,17 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           // (one shared-memory round trip instead of 5 NQ dependent ones:
           // the compiler cannot prove that the five arrays do not alias).
           const int d1 = dir + 1, d2 = dir == 0 ? 2 : 0;
-          Real* tn = tend + (1 + dir) * VS;
-          Real* tt1 = tend + (1 + d1) * VS;
-          Real* tt2 = tend + (1 + d2) * VS;
-          Real* t4 = tend + 4 * VS;
+          Real* tn = tslab + (1 + dir) * TV;
+          Real* tt1 = tslab + (1 + d1) * TV;
+          Real* tt2 = tslab + (1 + d2) * TV;
+          Real* t4 = tslab + 4 * TV;
           const Real scale = P.gain * P.metric[dir];
           if (SURF || dir != 0 || read_out) {
             Real old[NQ][5];
 #pragma unroll
             for (int i = 0; i < NQ; ++i) {
               const int s = base + i * stride;
-              old[i][0] = tend[s];
+              old[i][0] = tslab[s];
               old[i][1] = tn[s];
               old[i][2] = tt1[s];
               old[i][3] = tt2[s];
@@ -716,7 +831,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
 #pragma unroll
           for (int i = 0; i < NQ; ++i) {
             const int s = base + i * stride;
-            tend[s] = acc[i][0];
+            tslab[s] = acc[i][0];
             tn[s] = acc[i][1];
             tt1[s] = acc[i][2];
             tt2[s] = acc[i][3];
@@ -760,7 +875,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     for (int k = 0; k < NQ; ++k) {
       const int s = zbase + k * ZS;
 #pragma unroll
-      for (int v = 0; v < 5; ++v) knew[k][v] = tend[v * VS + s];
+      for (int v = 0; v < 5; ++v) knew[k][v] = tslab[v * TV + s];
     }
     if (VOL) {
       // acc still lacks the z metric

@@ -200,8 +200,9 @@ public:
     gas_.half_over_R = Real(1) / (Real(2) * R);
 
     const size_t state_bytes = sizeof(Real) * size_t(ne_) * 5 * size_t(n3_);
-    CU(cudaMalloc(&q_, state_bytes ? state_bytes : 16));
-    CU(cudaMalloc(&k_, state_bytes ? state_bytes : 16));
+    // + 64: slack for the kernels' 16-byte rounded TMA bulk reads
+    CU(cudaMalloc(&q_, state_bytes + 64));
+    CU(cudaMalloc(&k_, state_bytes + 64));
     CU(cudaMemset(q_, 0, state_bytes));
     CU(cudaMemset(k_, 0, state_bytes));
     CU(alloc_copy(&phi_, d.phi, sizeof(Real) * size_t(ne_) * size_t(n3_)));
@@ -305,7 +306,7 @@ public:
     CU(cudaSetDevice(device_));
     if (!q_alt_) {
       const size_t state_bytes = sizeof(Real) * size_t(ne_) * 5 * size_t(n3_);
-      CU(cudaMalloc(&q_alt_, state_bytes ? state_bytes : 16));
+      CU(cudaMalloc(&q_alt_, state_bytes + 64));
     }
     const int rc = launch(kModeFused, 0, 1, a_old, a_new, b, q_alt_, with_source, stage, st);
     if (rc == ESDG_B200_OK) std::swap(q_, q_alt_); // the new state is current
@@ -493,7 +494,9 @@ private:
   }
 
   static cudaError_t alloc_copy_impl(void** dst, const void* src, size_t bytes) {
-    cudaError_t e = cudaMalloc(dst, bytes ? bytes : 16);
+    // 64 bytes of slack: the kernels' TMA bulk copies round their source
+    // range outwards to multiples of 16 bytes
+    cudaError_t e = cudaMalloc(dst, bytes + 64);
     if (e != cudaSuccess) return e;
     if (bytes && src) e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
     return e;
