@@ -172,18 +172,19 @@ struct Geo {
   }
 };
 
-// Shared-memory map of rhs_kernel (bytes). With an unpadded node layout (odd
-// NQ) the element slabs of q, phi and out are contiguous in HBM exactly as
-// the kernel wants them in shared memory, so they arrive by TMA bulk copies:
-// q and phi into the (still unused) front of the node-value arrays, out into
-// the tendency slab, which then uses the [element][variable][node] order of
-// the state registers. A slab starts at a multiple of sizeof(Real), not of
-// 16 B, in HBM: the copy starts up to 12 B early and the data sit at the same
-// offset in shared memory, hence the slack words.
+// Shared-memory map of rhs_kernel (bytes). The CTA's slabs of q and phi are
+// contiguous in HBM and arrive by TMA bulk copies in the (still unused) front
+// of the node-value arrays, from where every thread picks the raw values of
+// its z line. With an unpadded node layout (odd NQ) the old `out` arrives
+// the same way, straight in the tendency slab, which then uses the
+// [element][variable][node] order of the state registers. A slab starts at a
+// multiple of sizeof(Real), not of 16 B, in HBM: the copy starts up to 12 B
+// early and the data sit at the same offset in shared memory, hence the
+// slack words.
 template <class Real, int NQ, int EPB>
 struct SmemMap {
   using G = Geo<NQ>;
-  static constexpr bool kBulk = G::PX == NQ;
+  static constexpr bool kBulk = G::PX == NQ; // the slab can take `out` by bulk copy too
   static constexpr int VS = EPB * G::N3P;
   static constexpr size_t up16(size_t x) { return (x + 15) & ~size_t(15); }
   static constexpr size_t kStagePhi = up16(size_t(EPB) * 5 * G::N3 * sizeof(Real) + 16);
@@ -191,7 +192,7 @@ struct SmemMap {
   static constexpr size_t kTab = kTend + up16((size_t(5) * VS + 4) * sizeof(Real));
   static constexpr size_t kBar = kTab + up16(size_t(LogTab<Real>::kReals) * sizeof(Real));
   static constexpr size_t kBytes = kBar + 16;
-  static_assert(!kBulk || kStagePhi + up16(size_t(EPB) * G::N3 * sizeof(Real) + 16) <= kTend,
+  static_assert(kStagePhi + up16(size_t(EPB) * G::N3 * sizeof(Real) + 16) <= kTend,
                 "q and phi staging must fit in front of the slab");
 };
 
@@ -577,9 +578,10 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   const Real* pe = P.phi + eg * N3 + l;
   Real qv[NQ][5], ph[NQ], ltab[kLogTabRegs];
   static_assert(EPB * N2 * kLogTabRegs >= LogTab<Real>::kReals, "CTA too small for the table");
-  if (kBulk) {
-    // One thread moves the CTA's slabs of q, phi and (accumulate form) out
-    // with three TMA bulk copies; everybody else only waits on the mbarrier.
+  {
+    // One thread moves the CTA's slabs of q, phi and (accumulate form, odd
+    // NQ) out with TMA bulk copies; everybody else only waits on the
+    // mbarrier.
     if (tid == 0) mbar_init(mbar, 1);
     __syncthreads();
     if (tid == 0) {
@@ -587,41 +589,28 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
       const unsigned nel = left < EPB ? unsigned(left) : unsigned(EPB);
       const unsigned bq = (off_q + nel * 5 * N3 * unsigned(sizeof(Real)) + 15u) & ~15u;
       const unsigned bp = (off_p + nel * N3 * unsigned(sizeof(Real)) + 15u) & ~15u;
-      const unsigned bo =
-          read_out ? (off_o + nel * 5 * N3 * unsigned(sizeof(Real)) + 15u) & ~15u : 0u;
+      const unsigned bo = (kBulk && read_out)
+                              ? (off_o + nel * 5 * N3 * unsigned(sizeof(Real)) + 15u) & ~15u
+                              : 0u;
       mbar_expect_tx(mbar, bq + bp + bo);
       bulk_g2s(smem_raw, reinterpret_cast<const char*>(P.q + slab0) - off_q, bq, mbar);
       bulk_g2s(smem_raw + Map::kStagePhi, reinterpret_cast<const char*>(P.phi + e0 * N3) - off_p, bp,
                mbar);
-      if (read_out)
+      if (kBulk && read_out)
         bulk_g2s(smem_raw + Map::kTend, reinterpret_cast<const char*>(P.out + slab0) - off_o, bo,
                  mbar);
     }
     load_log_table(ltab, tid, EPB * N2);
-    if (!read_out && SURF && active) {
-      // the faces are the slab's first writers and touch surface nodes only
-#pragma unroll
-      for (int k = 0; k < NQ; ++k)
-#pragma unroll
-        for (int v = 0; v < 5; ++v) tslab[v * TV + zbase + k * ZS] = Real(0);
-    }
-  } else {
-    load_log_table(ltab, tid, EPB * N2);
     if (active) {
-#pragma unroll
-      for (int k = 0; k < NQ; ++k) {
-#pragma unroll
-        for (int v = 0; v < 5; ++v) qv[k][v] = qe[v * N3 + k * N2];
-        ph[k] = pe[k * N2];
-      }
-      if (read_out) {
+      if (!kBulk && read_out) {
+        // padded slab (even NQ): element-wise asynchronous copies
         const Real* oe = P.out + eg * (5 * N3) + l;
 #pragma unroll
         for (int k = 0; k < NQ; ++k)
 #pragma unroll
           for (int v = 0; v < 5; ++v)
             cp_async<sizeof(Real)>(&tslab[v * TV + zbase + k * ZS], oe + v * N3 + k * N2);
-      } else if (SURF) {
+      } else if (!read_out && SURF) {
         // the faces are the slab's first writers and touch surface nodes only
 #pragma unroll
         for (int k = 0; k < NQ; ++k)
@@ -652,7 +641,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // the logarithm's table (FP64): fetched behind the state loads, visible to
   // the CTA before the first logarithm
   store_log_table(logtab, ltab, tid, EPB * N2);
-  if (kBulk) {
+  {
     // the slabs have landed: every thread takes the raw values of its z line
     // out of the staging area, which the node values are about to overwrite
     mbar_wait(mbar, 0);
@@ -668,7 +657,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     }
   }
   ESDG_CLK();
-  if (sizeof(Real) == 8 || kBulk) __syncthreads();
+  __syncthreads();
   ESDG_CLK();
   if (active) {
     if (SURF && !VOL) { // surface-only kernel: registers to spare, fetch early
