@@ -218,7 +218,7 @@ template <> struct Tile<8, 8> { static constexpr int EPB = 1, MINB = 3; static c
 template <> struct Tile<2, 4> { static constexpr int EPB = 32, MINB = 4; static constexpr bool LEAN = false; };
 template <> struct Tile<3, 4> { static constexpr int EPB = 14, MINB = 4; static constexpr bool LEAN = false; };
 template <> struct Tile<4, 4> { static constexpr int EPB = 8, MINB = 4; static constexpr bool LEAN = false; };
-template <> struct Tile<5, 4> { static constexpr int EPB = 5, MINB = 4; static constexpr bool LEAN = false; };
+template <> struct Tile<5, 4> { static constexpr int EPB = 5, MINB = 5; static constexpr bool LEAN = false; };
 template <> struct Tile<6, 4> { static constexpr int EPB = 3, MINB = 4; static constexpr bool LEAN = false; };
 template <> struct Tile<7, 4> { static constexpr int EPB = 2, MINB = 4; static constexpr bool LEAN = false; };
 template <> struct Tile<8, 4> { static constexpr int EPB = 2, MINB = 2; static constexpr bool LEAN = false; };
