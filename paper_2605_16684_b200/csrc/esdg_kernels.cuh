@@ -223,21 +223,73 @@ template <> struct Tile<6, 4> { static constexpr int EPB = 3, MINB = 4; static c
 template <> struct Tile<7, 4> { static constexpr int EPB = 2, MINB = 4; static constexpr bool LEAN = false; };
 template <> struct Tile<8, 4> { static constexpr int EPB = 2, MINB = 2; static constexpr bool LEAN = false; };
 
+// Shared-memory layout of the nine node quantities: three arrays of PAIRS --
+// (rho/2, b), (log rho/2, log b), (phi/2, 1/(2b)) -- followed by the three
+// velocity arrays. A node is then six shared-memory instructions instead of
+// nine (three 128-bit, three 64-bit in FP64): the load/store pipe's
+// instruction queue, not its bandwidth, is what the flux kernels run short
+// of. The first pair and the velocities are what every pair flux uses twice
+// ("hot"), the other two pairs once ("cold", re-fetched per pair at the
+// highest orders).
+template <class Real>
+struct Pair2;
+template <>
+struct Pair2<double> {
+  using type = double2;
+};
+template <>
+struct Pair2<float> {
+  using type = float2;
+};
+enum { P_RB = 0, P_LOGS = 1, P_PHI = 2, P_COUNT = 3 }; // pair arrays; velocities follow
+
+template <class Real>
+__device__ __forceinline__ void load_hot(const Real* vals, int VS, int s, int dir, Node<Real>& n) {
+  using V2 = typename Pair2<Real>::type;
+  const int d1 = dir == 2 ? 0 : dir + 1;
+  const int d2 = d1 == 2 ? 0 : d1 + 1;
+  const V2 rb = reinterpret_cast<const V2*>(vals)[P_RB * VS + s];
+  n.hr = rb.x;
+  n.b = rb.y;
+  n.hun = vals[(2 * P_COUNT + dir) * VS + s];
+  n.hut1 = vals[(2 * P_COUNT + d1) * VS + s];
+  n.hut2 = vals[(2 * P_COUNT + d2) * VS + s];
+}
+template <class Real>
+__device__ __forceinline__ void load_cold(const Real* vals, int VS, int s, Node<Real>& n) {
+  using V2 = typename Pair2<Real>::type;
+  const V2 lg = reinterpret_cast<const V2*>(vals)[P_LOGS * VS + s];
+  const V2 ph = reinterpret_cast<const V2*>(vals)[P_PHI * VS + s];
+  n.hlr = lg.x;
+  n.lb = lg.y;
+  n.hphi = ph.x;
+  n.hib = ph.y;
+}
+template <class Real>
+__device__ __forceinline__ void store_node(Real* vals, int VS, int s, const Real (&nv)[V_COUNT]) {
+  using V2 = typename Pair2<Real>::type;
+  V2* pv = reinterpret_cast<V2*>(vals);
+  V2 t;
+  t.x = nv[V_HR];
+  t.y = nv[V_B];
+  pv[P_RB * VS + s] = t;
+  t.x = nv[V_HLR];
+  t.y = nv[V_LB];
+  pv[P_LOGS * VS + s] = t;
+  t.x = nv[V_HPHI];
+  t.y = nv[V_HIB];
+  pv[P_PHI * VS + s] = t;
+  vals[(2 * P_COUNT + 0) * VS + s] = nv[V_HU0];
+  vals[(2 * P_COUNT + 1) * VS + s] = nv[V_HU1];
+  vals[(2 * P_COUNT + 2) * VS + s] = nv[V_HU2];
+}
+
 template <class Real>
 __device__ __forceinline__ Node<Real> load_node(const Real* vals, int VS, int s,
                                                 int dir) {
   Node<Real> n;
-  const int d1 = dir == 2 ? 0 : dir + 1;
-  const int d2 = d1 == 2 ? 0 : d1 + 1;
-  n.hr = vals[V_HR * VS + s];
-  n.hun = vals[(V_HU0 + dir) * VS + s];
-  n.hut1 = vals[(V_HU0 + d1) * VS + s];
-  n.hut2 = vals[(V_HU0 + d2) * VS + s];
-  n.b = vals[V_B * VS + s];
-  n.hlr = vals[V_HLR * VS + s];
-  n.lb = vals[V_LB * VS + s];
-  n.hphi = vals[V_HPHI * VS + s];
-  n.hib = vals[V_HIB * VS + s];
+  load_hot(vals, VS, s, dir, n);
+  load_cold(vals, VS, s, n);
   return n;
 }
 
@@ -281,29 +333,15 @@ __device__ __forceinline__ void sweep_line(const RhsParams<Real, NQ>& P,
   // per line against 24 NQ (NQ-1) FP64 instructions).
   constexpr bool kLean = Tile<NQ, sizeof(Real)>::LEAN;
   Node<Real> nd[NQ];
-  const int d1l = dir == 2 ? 0 : dir + 1;
-  const int d2l = d1l == 2 ? 0 : d1l + 1;
 #pragma unroll
   for (int i = 0; i < NQ; ++i) {
-    if (kLean) {
-      const int sn = base + i * stride;
-      nd[i].hr = vals[V_HR * VS + sn];
-      nd[i].hun = vals[(V_HU0 + dir) * VS + sn];
-      nd[i].hut1 = vals[(V_HU0 + d1l) * VS + sn];
-      nd[i].hut2 = vals[(V_HU0 + d2l) * VS + sn];
-      nd[i].b = vals[V_B * VS + sn];
-    } else {
+    if (kLean)
+      load_hot(vals, VS, base + i * stride, dir, nd[i]);
+    else
       nd[i] = load_node(vals, VS, base + i * stride, dir);
-    }
   }
   auto cold = [&](int i) {
-    if (kLean) {
-      const int sn = base + i * stride;
-      nd[i].hlr = vals[V_HLR * VS + sn];
-      nd[i].lb = vals[V_LB * VS + sn];
-      nd[i].hphi = vals[V_HPHI * VS + sn];
-      nd[i].hib = vals[V_HIB * VS + sn];
-    }
+    if (kLean) load_cold(vals, VS, base + i * stride, nd[i]);
   };
   // diagonal: t_i -= 2 g_d D_ii F(q_i, q_i)  (kernels.hpp:170-188). D_ii
   // vanishes analytically at interior LGL nodes; the host flushes its
@@ -672,8 +710,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
 #pragma unroll
     for (int k = 0; k < NQ; ++k) {
       const int s = zbase + k * ZS;
-#pragma unroll
-      for (int j = 0; j < V_COUNT; ++j) vals[j * VS + s] = nvs[k][j];
+      store_node(vals, VS, s, nvs[k]);
     }
     const int bad = badmask ? __ffs(badmask) - 1 : -1;
     if (SURF && VOL) {
