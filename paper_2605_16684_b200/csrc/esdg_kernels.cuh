@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // Neighbour state of face lf, fetched one face ahead of its use so the
   // (mostly L2-resident) gather hides behind arithmetic. The six neighbour
   // codes were read at kernel start, so a fetch is one round trip, not two.
-  constexpr int FPI = VOL ? 2 : 1;
+  constexpr int FPI = 1;
   NbrRaw<Real> cur[FPI]; // the gathered neighbour trace(s) of the next face iteration
   auto fetch = [&](int lf, NbrRaw<Real>& r) {
     const int dir = lf >> 1, side = lf & 1;
@@ -703,8 +703,9 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
       if (FPI == 2) fetch(1, cur[FPI - 1]);
     }
     // The NQ nodes are independent and computed stage by stage so that their
-    // reciprocal and logarithm chains interleave. A non-physical node is
-    // only remembered here and reported after the loop.
+    // reciprocal and logarithm chains interleave (a rolled one-node-per-
+    // iteration loop has a fifth of the code but measured 3-6 % slower). A
+    // non-physical node is only remembered here and reported after the loop.
     Real nvs[NQ][V_COUNT], prs[NQ];
     const unsigned badmask = node_vals_line<Real, NQ>(qv, ph, P.gas.gm1, logtab, nvs, prs);
 #pragma unroll
@@ -740,10 +741,12 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // by the z-line owners in phase A). Faces of one direction share no node,
   // faces of different directions do (edges), hence the two barriers.
   if (SURF) {
-    // FPI faces per iteration: 2 = both faces of a direction as two
-    // interleaved streams (measured best inside the fused kernels), 1 = one
-    // face at a time (half the code per iteration; measured best for the
-    // surface-only kernel: 5.45 vs 5.65 ms at configs[1])
+    // FPI faces per iteration. 2 (both faces of a direction as two
+    // interleaved instruction streams) doubles the loop body; with 53 KB of
+    // kernel code and three CTAs in different phases per SM the instruction
+    // cache then costs more than the extra ILP gives: one face per
+    // iteration measured 2.3 % faster in the fused kernels and 4 % in the
+    // surface-only kernel.
 #pragma unroll 1
     for (int lf = 0; lf < 6; lf += FPI) {
       const int dir = lf >> 1, side0 = lf & 1;
