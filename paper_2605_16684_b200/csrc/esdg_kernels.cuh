@@ -204,24 +204,24 @@ struct SmemMap {
 // state (ptxas -v is checked in DESIGN.md).
 template <int NQ, int BYTES>
 struct Tile;
-template <> struct Tile<2, 8> { static constexpr int EPB = 32, MINB = 4; static constexpr bool LEAN = false; };
-template <> struct Tile<3, 8> { static constexpr int EPB = 14, MINB = 4; static constexpr bool LEAN = false; };
-template <> struct Tile<4, 8> { static constexpr int EPB = 8, MINB = 3; static constexpr bool LEAN = false; };
+template <> struct Tile<2, 8> { static constexpr int EPB = 32, MINB = 4; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
+template <> struct Tile<3, 8> { static constexpr int EPB = 14, MINB = 4; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
+template <> struct Tile<4, 8> { static constexpr int EPB = 8, MINB = 3; static constexpr int FPI = 2; static constexpr bool LEAN = false; };
 #ifndef ESDG_TUNE_EPB
 #define ESDG_TUNE_EPB 5
 #define ESDG_TUNE_MINB 3
 #endif
-template <> struct Tile<5, 8> { static constexpr int EPB = ESDG_TUNE_EPB, MINB = ESDG_TUNE_MINB; static constexpr bool LEAN = false; };
-template <> struct Tile<6, 8> { static constexpr int EPB = 3, MINB = 2; static constexpr bool LEAN = false; };
-template <> struct Tile<7, 8> { static constexpr int EPB = 2, MINB = 2; static constexpr bool LEAN = true; };
-template <> struct Tile<8, 8> { static constexpr int EPB = 1, MINB = 3; static constexpr bool LEAN = true; };
-template <> struct Tile<2, 4> { static constexpr int EPB = 32, MINB = 4; static constexpr bool LEAN = false; };
-template <> struct Tile<3, 4> { static constexpr int EPB = 14, MINB = 4; static constexpr bool LEAN = false; };
-template <> struct Tile<4, 4> { static constexpr int EPB = 8, MINB = 4; static constexpr bool LEAN = false; };
-template <> struct Tile<5, 4> { static constexpr int EPB = 5, MINB = 5; static constexpr bool LEAN = false; };
-template <> struct Tile<6, 4> { static constexpr int EPB = 3, MINB = 4; static constexpr bool LEAN = false; };
-template <> struct Tile<7, 4> { static constexpr int EPB = 2, MINB = 4; static constexpr bool LEAN = false; };
-template <> struct Tile<8, 4> { static constexpr int EPB = 2, MINB = 2; static constexpr bool LEAN = false; };
+template <> struct Tile<5, 8> { static constexpr int EPB = ESDG_TUNE_EPB, MINB = ESDG_TUNE_MINB; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
+template <> struct Tile<6, 8> { static constexpr int EPB = 3, MINB = 2; static constexpr int FPI = 2; static constexpr bool LEAN = false; };
+template <> struct Tile<7, 8> { static constexpr int EPB = 2, MINB = 2; static constexpr int FPI = 2; static constexpr bool LEAN = true; };
+template <> struct Tile<8, 8> { static constexpr int EPB = 1, MINB = 3; static constexpr int FPI = 2; static constexpr bool LEAN = true; };
+template <> struct Tile<2, 4> { static constexpr int EPB = 32, MINB = 4; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
+template <> struct Tile<3, 4> { static constexpr int EPB = 14, MINB = 4; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
+template <> struct Tile<4, 4> { static constexpr int EPB = 8, MINB = 4; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
+template <> struct Tile<5, 4> { static constexpr int EPB = 5, MINB = 5; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
+template <> struct Tile<6, 4> { static constexpr int EPB = 3, MINB = 4; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
+template <> struct Tile<7, 4> { static constexpr int EPB = 2, MINB = 4; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
+template <> struct Tile<8, 4> { static constexpr int EPB = 2, MINB = 2; static constexpr int FPI = 2; static constexpr bool LEAN = false; };
 
 // Shared-memory layout of the nine node quantities: three arrays of PAIRS --
 // (rho/2, b), (log rho/2, log b), (phi/2, 1/(2b)) -- followed by the three
@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // Neighbour state of face lf, fetched one face ahead of its use so the
   // (mostly L2-resident) gather hides behind arithmetic. The six neighbour
   // codes were read at kernel start, so a fetch is one round trip, not two.
-  constexpr int FPI = 1;
+  constexpr int FPI = Tile<NQ, sizeof(Real)>::FPI;
   NbrRaw<Real> cur[FPI]; // the gathered neighbour trace(s) of the next face iteration
   auto fetch = [&](int lf, NbrRaw<Real>& r) {
     const int dir = lf >> 1, side = lf & 1;
@@ -741,12 +741,13 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // by the z-line owners in phase A). Faces of one direction share no node,
   // faces of different directions do (edges), hence the two barriers.
   if (SURF) {
-    // FPI faces per iteration. 2 (both faces of a direction as two
-    // interleaved instruction streams) doubles the loop body; with 53 KB of
-    // kernel code and three CTAs in different phases per SM the instruction
-    // cache then costs more than the extra ILP gives: one face per
-    // iteration measured 2.3 % faster in the fused kernels and 4 % in the
-    // surface-only kernel.
+    // FPI faces per iteration (Tile<>::FPI). 2 = both faces of a direction as
+    // two interleaved instruction streams: more ILP, but twice the loop
+    // body. Where three or more CTAs in different phases share an SM the
+    // instruction cache decides (N <= 4 in FP64: with FPI = 2, 10 % of the
+    // stall samples were `no_instruction`, 85 % of them on the first
+    // instruction of a 128-byte code line; 2 % with FPI = 1); the one or two
+    // fat CTAs per SM of the high orders prefer the ILP.
 #pragma unroll 1
     for (int lf = 0; lf < 6; lf += FPI) {
       const int dir = lf >> 1, side0 = lf & 1;
