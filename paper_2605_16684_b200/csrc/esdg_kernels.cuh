@@ -151,6 +151,19 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// TMA bulk copy shared -> global (bulk async-group completion).
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store_commit_and_wait_read() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
@@ -875,37 +888,46 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
 
   ESDG_CLK();
   // ---- commit: slab (old out, faces, x, y) + registers (z) on the z line ----
+  // acc: rotated frame of z: normal -> var 3, t1 = x -> 1, t2 = y -> 2
+  // commit (solver.hpp:199-223), one z line per thread. With the TMA slab
+  // layout (odd NQ) the results go back into shared memory -- k in place in
+  // the slab, q_next into the dead front of the node-value arrays, both in
+  // the state registers' [element][variable][node] order -- and one thread
+  // ships each slab with a bulk store: the 16-byte-aligned interior by TMA,
+  // the at most three Reals in front of / behind it by ordinary stores.
+  // Otherwise every thread stores its z line, coalesced over l. Global loads
+  // (only the fused stage update and the Coriolis source need any) are issued
+  // before the first store: the compiler cannot prove that out / q / q_next
+  // do not alias.
+  const bool update = VOL && P.q_next != nullptr;
+  const bool source = VOL && P.with_source != 0;
+  const unsigned off_n =
+      update ? unsigned(reinterpret_cast<unsigned long long>(P.q_next + slab0) & 15u) : 0u;
+  Real knew[NQ][5], qc[NQ][5];
   if (active) {
-    // acc: rotated frame of z: normal -> var 3, t1 = x -> 1, t2 = y -> 2
-    // commit (solver.hpp:199-223), one z line per thread, coalesced over l.
-    // Global loads (only the fused stage update and the Coriolis source need
-    // any) are issued before the first store: the compiler cannot prove that
-    // out / q / q_next do not alias.
     const Real* __restrict__ qe = P.q + eg * (5 * N3) + l;
-    Real* __restrict__ oe = P.out + eg * (5 * N3) + l;
-    const bool update = VOL && P.q_next != nullptr;
-    const bool source = VOL && P.with_source != 0;
-    Real qv[NQ][5], cf = Real(0);
+    Real cf = Real(0);
     if (update) {
 #pragma unroll
       for (int k = 0; k < NQ; ++k)
 #pragma unroll
-        for (int v = 0; v < 5; ++v) qv[k][v] = qe[v * N3 + k * N2];
+        for (int v = 0; v < 5; ++v) qc[k][v] = qe[v * N3 + k * N2];
     } else if (source) {
       // coriolis_source (physics.hpp:297-306) only needs the momenta
 #pragma unroll
       for (int k = 0; k < NQ; ++k) {
-        qv[k][1] = qe[1 * N3 + k * N2];
-        qv[k][2] = qe[2 * N3 + k * N2];
+        qc[k][1] = qe[1 * N3 + k * N2];
+        qc[k][2] = qe[2 * N3 + k * N2];
       }
     }
     if (source) cf = P.cor_f[P.ylevel[eg] * NQ + l1];
-    Real knew[NQ][5];
+    if (VOL || !kBulk) {
 #pragma unroll
-    for (int k = 0; k < NQ; ++k) {
-      const int s = zbase + k * ZS;
+      for (int k = 0; k < NQ; ++k) {
+        const int s = zbase + k * ZS;
 #pragma unroll
-      for (int v = 0; v < 5; ++v) knew[k][v] = tslab[v * TV + s];
+        for (int v = 0; v < 5; ++v) knew[k][v] = tslab[v * TV + s];
+      }
     }
     if (VOL) {
       // acc still lacks the z metric
@@ -923,8 +945,8 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         const Real gcf = P.gain * cf;
 #pragma unroll
         for (int k = 0; k < NQ; ++k) {
-          knew[k][1] = fma_(gcf, qv[k][2], knew[k][1]);
-          knew[k][2] = fma_(-gcf, qv[k][1], knew[k][2]);
+          knew[k][1] = fma_(gcf, qc[k][2], knew[k][1]);
+          knew[k][2] = fma_(-gcf, qc[k][1], knew[k][2]);
         }
       }
 #pragma unroll
@@ -932,20 +954,74 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
 #pragma unroll
         for (int v = 0; v < 5; ++v) knew[k][v] = P.fin * knew[k][v];
     }
-#pragma unroll
-    for (int k = 0; k < NQ; ++k)
-#pragma unroll
-      for (int v = 0; v < 5; ++v) oe[v * N3 + k * N2] = knew[k][v];
-    if (update) {
-      // LSRK register update folded into the same pass (Solver::axpy,
-      // solver.hpp:342-353): q_next = q + b k. q is double buffered
-      // because neighbouring CTAs still read this element's faces.
-      Real* __restrict__ qn = P.q_next + eg * (5 * N3) + l;
+    if (!kBulk) {
+      Real* __restrict__ oe = P.out + eg * (5 * N3) + l;
 #pragma unroll
       for (int k = 0; k < NQ; ++k)
 #pragma unroll
-        for (int v = 0; v < 5; ++v)
-          qn[v * N3 + k * N2] = qv[k][v] + P.b_upd * knew[k][v];
+        for (int v = 0; v < 5; ++v) oe[v * N3 + k * N2] = knew[k][v];
+      if (update) {
+        // LSRK register update folded into the same pass (Solver::axpy,
+        // solver.hpp:342-353): q_next = q + b k. q is double buffered
+        // because neighbouring CTAs still read this element's faces.
+        Real* __restrict__ qn = P.q_next + eg * (5 * N3) + l;
+#pragma unroll
+        for (int k = 0; k < NQ; ++k)
+#pragma unroll
+          for (int v = 0; v < 5; ++v)
+            qn[v * N3 + k * N2] = qc[k][v] + P.b_upd * knew[k][v];
+      }
+    }
+  }
+  if (kBulk) {
+    // q_next goes where other threads may still be reading node values for
+    // their z sweep: wait for them
+    if (update) __syncthreads();
+    Real* stage_n = reinterpret_cast<Real*>(smem_raw + off_n);
+    if (active) {
+      if (VOL) {
+#pragma unroll
+        for (int k = 0; k < NQ; ++k)
+#pragma unroll
+          for (int v = 0; v < 5; ++v) tslab[v * TV + zbase + k * ZS] = knew[k][v];
+      }
+      if (update) {
+#pragma unroll
+        for (int k = 0; k < NQ; ++k)
+#pragma unroll
+          for (int v = 0; v < 5; ++v)
+            stage_n[(e * 5 + v) * N3 + l + k * N2] = qc[k][v] + P.b_upd * knew[k][v];
+      }
+    }
+    fence_proxy_async_smem(); // generic-proxy writes -> visible to the TMA engine
+    __syncthreads();
+    const long long left = P.ne - e0;
+    const unsigned nel = left < EPB ? unsigned(left) : unsigned(EPB);
+    const unsigned bytes = nel * 5 * N3 * unsigned(sizeof(Real));
+    // slab `which`: 0 = out from the tendency slab, 1 = q_next from the staging area
+    auto ship = [&](int which, bool interior) {
+      char* g = reinterpret_cast<char*>(which == 0 ? P.out + slab0 : P.q_next + slab0);
+      const char* sm = reinterpret_cast<const char*>(smem_raw) +
+                       (which == 0 ? Map::kTend + off_o : size_t(off_n));
+      const unsigned head = (16u - unsigned(reinterpret_cast<unsigned long long>(g) & 15u)) & 15u;
+      const unsigned body = (bytes - head) & ~15u;
+      if (interior) {
+        bulk_s2g(g + head, sm + head, body);
+      } else {
+        for (unsigned o = 0; o < head; o += sizeof(Real))
+          *reinterpret_cast<Real*>(g + o) = *reinterpret_cast<const Real*>(sm + o);
+        for (unsigned o = head + body; o < bytes; o += sizeof(Real))
+          *reinterpret_cast<Real*>(g + o) = *reinterpret_cast<const Real*>(sm + o);
+      }
+    };
+    if (tid == 0) {
+      ship(0, true);
+      if (update) ship(1, true);
+      bulk_store_commit_and_wait_read();
+    } else if (tid == 32) {
+      ship(0, false);
+    } else if (tid == 64 && update) {
+      ship(1, false);
     }
   }
 #ifdef ESDG_TUNE_PHASE_CLOCKS
