@@ -336,6 +336,13 @@ int esdg_b200_solver_init_case(esdg_b200_solver* s, int case_id,
 /* state()/k register as host StateField arrays of the LOCAL element range */
 int esdg_b200_solver_set_state(esdg_b200_solver* s, int reg, const void* host);
 int esdg_b200_solver_get_state(esdg_b200_solver* s, int reg, void* host);
+/* get_state into host_out and set_state from host_in in one full-duplex,
+ * chunk-pipelined pass (the upload of a chunk waits for its own download
+ * only): what a coupled driver does between two steps when it hands state()
+ * to host code and takes it back. host_in may alias host_out. Pinned host
+ * memory is needed for the two directions to overlap. */
+int esdg_b200_solver_swap_state(esdg_b200_solver* s, int reg, const void* host_in,
+                                void* host_out);
 /* phi() (solver.hpp:79), local range */
 int esdg_b200_solver_get_phi(esdg_b200_solver* s, void* host);
 

@@ -131,6 +131,7 @@ SIGNATURES = {
     "esdg_b200_solver_init_case": (_i, [_vp, _i, C.c_uint64, _dp]),
     "esdg_b200_solver_set_state": (_i, [_vp, _i, _vp]),
     "esdg_b200_solver_get_state": (_i, [_vp, _i, _vp]),
+    "esdg_b200_solver_swap_state": (_i, [_vp, _i, _vp, _vp]),
     "esdg_b200_solver_get_phi": (_i, [_vp, _vp]),
     "esdg_b200_solver_assemble_rhs": (_i, [_vp, _vp, _vp, _d, _d]),
     "esdg_b200_solver_volume_rhs": (_i, [_vp, _vp, _vp]),
@@ -393,6 +394,18 @@ class GpuSolver:
         out = np.empty(self.shape, self.dtype)
         self._chk(lib().esdg_b200_solver_get_state(self.h, reg, out.ctypes.data_as(_vp)))
         return out
+
+    def swap_state(self, q_in, q_out=None, reg=REG_Q):
+        """Downloads the register into q_out and refills it from q_in in one
+        full-duplex pass; q_out defaults to a new array, may be q_in itself."""
+        q_in = np.ascontiguousarray(q_in, self.dtype)
+        assert q_in.shape == self.shape
+        if q_out is None:
+            q_out = np.empty(self.shape, self.dtype)
+        assert q_out.shape == self.shape and q_out.dtype == self.dtype and q_out.flags.c_contiguous
+        self._chk(lib().esdg_b200_solver_swap_state(self.h, reg, q_in.ctypes.data_as(_vp),
+                                                    q_out.ctypes.data_as(_vp)))
+        return q_out
 
     def get_phi(self):
         out = np.empty((self.shape[0], self.n3), self.dtype)

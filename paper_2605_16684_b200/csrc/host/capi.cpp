@@ -251,6 +251,10 @@ int esdg_b200_solver_set_state(esdg_b200_solver* s, int reg, const void* host) {
   CORE(s);
   return c.set_state(reg, host);
 }
+int esdg_b200_solver_swap_state(esdg_b200_solver* s, int reg, const void* host_in, void* host_out) {
+  CORE(s);
+  return c.swap_state(reg, host_in, host_out);
+}
 int esdg_b200_solver_get_state(esdg_b200_solver* s, int reg, void* host) {
   CORE(s);
   return c.get_state(reg, host);

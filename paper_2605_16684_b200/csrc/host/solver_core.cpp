@@ -313,6 +313,43 @@ int SolverCore::get_state(int reg, void* host) {
   return ESDG_B200_OK;
 }
 
+// get_state + set_state in one full-duplex pass: the register is downloaded
+// to host_out and refilled from host_in chunk by chunk, the upload of chunk c
+// queued behind its own download only, so that on a PCIe link both directions
+// run at once (a coupled driver that hands the state to host physics and
+// takes it back each step). host_in may alias host_out: a chunk is then
+// uploaded after it has been downloaded. Host memory should be pinned.
+int SolverCore::swap_state(int reg, const void* host_in, void* host_out) {
+  if (!host_in || !host_out) return ESDG_B200_BADARG;
+  const size_t per = size_t(opt_.precision) * 5 * size_t(n3_);
+  const int64_t chunk = std::max<int64_t>(1, (int64_t(32) << 20) / int64_t(per));
+  for (auto& ls : shards_) {
+    CU(cudaSetDevice(ls.dev->device()));
+    cudaStream_t down = ls.dev->stream(), up = ls.comm ? ls.comm : ls.dev->stream();
+    cudaEvent_t ev = nullptr;
+    CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    const size_t base = size_t(ls.begin - local_begin_) * per;
+    int rc = ESDG_B200_OK;
+    for (int64_t first = 0; first < ls.end - ls.begin && rc == ESDG_B200_OK; first += chunk) {
+      const int64_t count = std::min(chunk, ls.end - ls.begin - first);
+      const size_t off = base + size_t(first) * per;
+      rc = ls.dev->download(reg, static_cast<char*>(host_out) + off, first, count, down, true);
+      if (rc != ESDG_B200_OK) break;
+      if (cudaEventRecord(ev, down) != cudaSuccess || cudaStreamWaitEvent(up, ev, 0) != cudaSuccess) {
+        rc = ESDG_B200_CUDA;
+        break;
+      }
+      rc = ls.dev->upload(reg, static_cast<const char*>(host_in) + off, first, count, up, true);
+    }
+    const cudaError_t e1 = cudaStreamSynchronize(down), e2 = cudaStreamSynchronize(up);
+    cudaEventDestroy(ev);
+    if (rc != ESDG_B200_OK) return rc;
+    if (e1 != cudaSuccess) return cuda_fail(e1, "swap_state");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "swap_state");
+  }
+  return ESDG_B200_OK;
+}
+
 int SolverCore::get_phi(void* host) const {
   if (!host) return ESDG_B200_BADARG;
   const double g = opt_.gas.gravity;

@@ -55,6 +55,7 @@ public:
   int init_case(int case_id, uint64_t iparam, const double* dparam);
   int set_state(int reg, const void* host);
   int get_state(int reg, void* host);
+  int swap_state(int reg, const void* host_in, void* host_out);
   int get_phi(void* host) const;
 
   int assemble_rhs_host(const void* q, void* out, double a_old, double a_new,

@@ -414,3 +414,19 @@ def test_runner_outputs(tmp_path):
     assert res["mass_drift"] <= 1e-14 and res["energy_drift"] <= 1e-14
     assert all(row[3] <= 0.0 for row in res["entropy"])
     assert "# status = ok" in (tmp_path / "manifest.txt").read_text()
+
+
+def test_swap_state_equals_get_then_set(port):
+    """esdg_b200_solver_swap_state: the register goes to the host and is
+    refilled in one full-duplex pass; same result as get_state followed by
+    set_state, also with several partitions and with aliased buffers."""
+    for ranks in (1, 3):
+        o, g = make(port, "bubble", (2, False), 3, ranks=ranks)
+        q0 = o.init_case(po.CASE_BUBBLE_SMOOTH).copy()
+        g.set_state(q0)
+        q1 = q0 * 1.25
+        out = g.swap_state(q1)
+        assert np.array_equal(out, q0) and np.array_equal(g.get_state(), q1)
+        buf = q0.copy()                      # aliased: download, then upload the same chunk
+        g.swap_state(buf, buf)
+        assert np.array_equal(buf, q1) and np.array_equal(g.get_state(), q1)
