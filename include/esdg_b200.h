@@ -162,6 +162,29 @@ int esdg_b200_shard_rhs_fused(esdg_b200_shard* s, int src, int dst,
 int esdg_b200_shard_stage_fused(esdg_b200_shard* s, double a_old, double a_new,
                                 double b, int stage, void* stream);
 
+/* The one-pass kernels restricted to a part of the partition, so that they
+ * overlap the halo exchange the way the reference's volume phase does
+ * (rhs_job, solver.hpp:259-294: volume -> wait -> ghost faces). An element
+ * group is the run of consecutive elements one CTA owns; PART_INTERIOR are
+ * the groups without a ghost face (they never read the receive buffer),
+ * PART_BOUNDARY the rest. Order per RHS: pack -> start the transfer ->
+ * PART_INTERIOR -> traces have landed -> PART_BOUNDARY. INTERIOR followed by
+ * BOUNDARY is bitwise the PART_ALL result; stage_fused_part swaps the state
+ * buffers after PART_BOUNDARY (or PART_ALL), so both parts read the old q. */
+enum {
+  ESDG_B200_PART_ALL = 0,
+  ESDG_B200_PART_INTERIOR = 1,
+  ESDG_B200_PART_BOUNDARY = 2
+};
+int esdg_b200_shard_rhs_fused_part(esdg_b200_shard* s, int src, int dst,
+                                   double a_old, double a_new, int stage,
+                                   int part, void* stream);
+int esdg_b200_shard_stage_fused_part(esdg_b200_shard* s, double a_old,
+                                     double a_new, double b, int stage,
+                                     int part, void* stream);
+/* number of elements in a part (diagnostic: how much work hides the halo) */
+int esdg_b200_shard_part_elements(esdg_b200_shard* s, int part, int64_t* count);
+
 /* K3: q <- q + b k. Replaces Solver::axpy (solver.hpp:342-353). */
 int esdg_b200_shard_axpy(esdg_b200_shard* s, double b, void* stream);
 
@@ -311,6 +334,15 @@ int esdg_b200_solver_create_distributed(
 void esdg_b200_solver_destroy(esdg_b200_solver* s);
 
 int esdg_b200_solver_set_path(esdg_b200_solver* s, int path);
+/* PATH_FUSED / PATH_STAGE with several partitions: on (default) runs the
+ * element groups without a ghost face while the traces travel and the rest
+ * after they have landed (rhs_job's order, solver.hpp:259-294); off waits for
+ * the traces first and launches one kernel. Results are bitwise the same.
+ * interior / total (may be null): elements of this process' partitions that
+ * hide the exchange / all of them. */
+int esdg_b200_solver_set_overlap(esdg_b200_solver* s, int on);
+int esdg_b200_solver_overlap_elements(esdg_b200_solver* s, int64_t* interior,
+                                      int64_t* total);
 int esdg_b200_solver_set_settings(esdg_b200_solver* s,
                                   const esdg_b200_settings* settings);
 int64_t esdg_b200_solver_local_begin(const esdg_b200_solver* s);

@@ -95,6 +95,9 @@ SIGNATURES = {
     "esdg_b200_shard_surface": (_i, [_vp, _i, _i, _d, _i, _vp]),
     "esdg_b200_shard_rhs_fused": (_i, [_vp, _i, _i, _d, _d, _i, _vp]),
     "esdg_b200_shard_stage_fused": (_i, [_vp, _d, _d, _d, _i, _vp]),
+    "esdg_b200_shard_rhs_fused_part": (_i, [_vp, _i, _i, _d, _d, _i, _i, _vp]),
+    "esdg_b200_shard_stage_fused_part": (_i, [_vp, _d, _d, _d, _i, _i, _vp]),
+    "esdg_b200_shard_part_elements": (_i, [_vp, _i, C.POINTER(C.c_int64)]),
     "esdg_b200_shard_axpy": (_i, [_vp, _d, _vp]),
     "esdg_b200_shard_check": (_i, [_vp, _vp, C.POINTER(Error)]),
     "esdg_b200_shard_reduce": (_i, [_vp, _i, _i, _i, _dp, _dp, _d, _dp, C.POINTER(C.c_int32)]),
@@ -119,6 +122,8 @@ SIGNATURES = {
                                                  C.POINTER(_vp)]),
     "esdg_b200_solver_destroy": (None, [_vp]),
     "esdg_b200_solver_set_path": (_i, [_vp, _i]),
+    "esdg_b200_solver_set_overlap": (_i, [_vp, _i]),
+    "esdg_b200_solver_overlap_elements": (_i, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "esdg_b200_solver_set_settings": (_i, [_vp, C.POINTER(Settings)]),
     "esdg_b200_solver_local_begin": (_i64, [_vp]),
     "esdg_b200_solver_local_end": (_i64, [_vp]),
@@ -375,6 +380,15 @@ class GpuSolver:
 
     def set_path(self, path):
         self._chk(lib().esdg_b200_solver_set_path(self.h, path))
+
+    def set_overlap(self, on):
+        self._chk(lib().esdg_b200_solver_set_overlap(self.h, 1 if on else 0))
+
+    def overlap_elements(self):
+        """(elements whose work hides the halo exchange, all local elements)"""
+        a, b = C.c_int64(0), C.c_int64(0)
+        self._chk(lib().esdg_b200_solver_overlap_elements(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def set_settings(self, settings: Settings):
         self._chk(lib().esdg_b200_solver_set_settings(self.h, C.byref(settings)))

@@ -8,7 +8,8 @@ namespace esdg_b200 {
 
 namespace {
 template <class Real, int NQ, bool VOL, bool SURF>
-cudaError_t launch_one(const dev::RhsParams<Real, NQ>& P, cudaStream_t stream) {
+cudaError_t launch_one(const dev::RhsParams<Real, NQ>& P, long long n_groups,
+                       cudaStream_t stream) {
   constexpr int EPB = dev::Tile<NQ, sizeof(Real)>::EPB;
   constexpr int MINB = dev::Tile<NQ, sizeof(Real)>::MINB;
   constexpr int T = EPB * NQ * NQ;
@@ -25,7 +26,8 @@ cudaError_t launch_one(const dev::RhsParams<Real, NQ>& P, cudaStream_t stream) {
   });
   if (attr_err != cudaSuccess) return attr_err;
   if (P.ne <= 0) return cudaSuccess;
-  const long long blocks = (P.ne + EPB - 1) / EPB;
+  const long long blocks = P.groups ? n_groups : (P.ne + EPB - 1) / EPB;
+  if (blocks <= 0) return cudaSuccess;
   kern<<<dim3(unsigned(blocks)), dim3(T), smem, stream>>>(P);
   return cudaGetLastError();
 }
@@ -33,11 +35,11 @@ cudaError_t launch_one(const dev::RhsParams<Real, NQ>& P, cudaStream_t stream) {
 
 template <class Real, int NQ>
 cudaError_t launch_rhs(int mode, const dev::RhsParams<Real, NQ>& P,
-                       cudaStream_t stream) {
+                       long long n_groups, cudaStream_t stream) {
   switch (mode) {
-    case kModeVolume: return launch_one<Real, NQ, true, false>(P, stream);
-    case kModeSurface: return launch_one<Real, NQ, false, true>(P, stream);
-    case kModeFused: return launch_one<Real, NQ, true, true>(P, stream);
+    case kModeVolume: return launch_one<Real, NQ, true, false>(P, n_groups, stream);
+    case kModeSurface: return launch_one<Real, NQ, false, true>(P, n_groups, stream);
+    case kModeFused: return launch_one<Real, NQ, true, true>(P, n_groups, stream);
   }
   return cudaErrorInvalidValue;
 }
@@ -65,7 +67,7 @@ void rhs_launch_shape(int* threads, int* epb, size_t* smem_bytes) {
 
 #define ESDG_INSTANTIATE(REAL, NQ)                                             \
   template cudaError_t launch_rhs<REAL, NQ>(                                   \
-      int, const dev::RhsParams<REAL, NQ>&, cudaStream_t);                     \
+      int, const dev::RhsParams<REAL, NQ>&, long long, cudaStream_t);          \
   template cudaError_t launch_pack<REAL, NQ>(const REAL*, const int32_t*,      \
                                              const int32_t*, REAL*, long long, \
                                              cudaStream_t);                    \

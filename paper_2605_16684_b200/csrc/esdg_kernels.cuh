@@ -65,6 +65,10 @@ struct RhsParams {
   const Real* ghost_phi;
   const int32_t* ylevel;
   const Real* cor_f;
+  // CTA -> element group (EPB consecutive elements): null = blockIdx.x. The
+  // interior / boundary lists let the one-pass kernels overlap the halo
+  // exchange the way the reference's volume phase does (solver.hpp:259-262).
+  const int32_t* groups;
   unsigned long long* flag;
   FlagRecord* flag_records;
   long long ne;
@@ -538,7 +542,8 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(smem_raw + Map::kBar);
 
   const int tid = threadIdx.x;
-  const long long e0 = static_cast<long long>(blockIdx.x) * EPB;
+  const long long e0 =
+      static_cast<long long>(P.groups ? P.groups[blockIdx.x] : int32_t(blockIdx.x)) * EPB;
 #ifdef ESDG_TUNE_PHASE_CLOCKS
   long long tclk[10];
   int nclk = 0;
@@ -676,7 +681,11 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // instead of one prefetch instruction per 128 bytes -- those brought in
   // single sectors, and a quarter of the demand loads still missed L2
   {
-    const long long en = e0 + static_cast<long long>(P.prefetch_ctas) * EPB;
+    long long en = e0 + static_cast<long long>(P.prefetch_ctas) * EPB;
+    if (P.groups) {
+      const unsigned nb = blockIdx.x + unsigned(P.prefetch_ctas);
+      en = nb < gridDim.x ? static_cast<long long>(P.groups[nb]) * EPB : P.ne;
+    }
     if (tid < 3 && en + EPB <= P.ne && (tid < 2 || read_out)) {
       const char* base = tid == 0   ? reinterpret_cast<const char*>(P.q + en * (5 * N3))
                          : tid == 1 ? reinterpret_cast<const char*>(P.phi + en * N3)

@@ -16,9 +16,11 @@ struct RhsParams;
 
 enum RhsMode { kModeVolume = 0, kModeSurface = 1, kModeFused = 2 };
 
+// P.groups == null: one CTA per EPB consecutive elements of [0, P.ne);
+// otherwise n_groups CTAs, CTA i working on group P.groups[i].
 template <class Real, int NQ>
 cudaError_t launch_rhs(int mode, const dev::RhsParams<Real, NQ>& P,
-                       cudaStream_t stream);
+                       long long n_groups, cudaStream_t stream);
 
 template <class Real, int NQ>
 cudaError_t launch_pack(const Real* q, const int32_t* send_elem,

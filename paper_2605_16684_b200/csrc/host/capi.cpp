@@ -218,6 +218,16 @@ void esdg_b200_solver_destroy(esdg_b200_solver* s) {
 #define CORE(s) if (!(s)) return ESDG_B200_BADARG; SolverCore& c = *(s)->core
 
 int esdg_b200_solver_set_path(esdg_b200_solver* s, int path) { CORE(s); return c.set_path(path); }
+int esdg_b200_solver_set_overlap(esdg_b200_solver* s, int on) {
+  CORE(s);
+  c.set_overlap(on != 0);
+  return ESDG_B200_OK;
+}
+int esdg_b200_solver_overlap_elements(esdg_b200_solver* s, int64_t* interior, int64_t* total) {
+  CORE(s);
+  c.overlap_elements(interior, total);
+  return ESDG_B200_OK;
+}
 int esdg_b200_solver_set_settings(esdg_b200_solver* s, const esdg_b200_settings* st) {
   CORE(s);
   return st ? c.set_settings(*st) : ESDG_B200_BADARG;

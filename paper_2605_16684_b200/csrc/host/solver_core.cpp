@@ -266,6 +266,17 @@ int SolverCore::set_path(int path) {
   return ESDG_B200_OK;
 }
 
+void SolverCore::overlap_elements(int64_t* interior, int64_t* total) {
+  int64_t in = 0, all = 0;
+  for (auto& ls : shards_) {
+    all += ls.dev->n_elements();
+    in += ls.halo.peers.empty() ? ls.dev->n_elements()
+                                : ls.dev->part_elements(ESDG_B200_PART_INTERIOR);
+  }
+  if (interior) *interior = in;
+  if (total) *total = all;
+}
+
 int SolverCore::set_settings(const esdg_b200_settings& s) {
   // the Coriolis table depends on (mode, f0, beta, y0): re-create is the
   // simple route; dissipation alone is a flag flip
@@ -537,26 +548,40 @@ int SolverCore::rhs(int src, int dst, double a_old, double a_new,
   const int source = (with_source && opt_.settings.coriolis_mode != 0) ? 1 : 0;
   if (halo) RC(exchange_begin(src));
   if (path_ != ESDG_B200_PATH_SPLIT && !volume_only) {
+    // one-pass kernel: the element groups without a ghost face run while the
+    // traces travel, the others after they have landed (solver.hpp:259-294)
+    const bool split = halo && overlap_;
+    for (auto& ls : shards_)
+      RC(timed(ls, kClsVolume, [&] {
+        return ls.dev->rhs(kModeFused, src, dst, a_old, a_new, source, stage,
+                           split && !ls.halo.peers.empty() ? ESDG_B200_PART_INTERIOR
+                                                           : ESDG_B200_PART_ALL,
+                           nullptr);
+      }));
     if (halo) RC(exchange_end());
     for (auto& ls : shards_) {
-      RC(timed(ls, kClsVolume, [&] {
-        return ls.dev->rhs(kModeFused, src, dst, a_old, a_new, source, stage, nullptr);
-      }));
-      if (halo && !ls.halo.peers.empty()) CU(cudaEventRecord(ls.ev_surf, ls.dev->stream()));
+      if (!halo || ls.halo.peers.empty()) continue;
+      if (split)
+        RC(timed(ls, kClsVolume, [&] {
+          return ls.dev->rhs(kModeFused, src, dst, a_old, a_new, source, stage,
+                             ESDG_B200_PART_BOUNDARY, nullptr);
+        }));
+      CU(cudaSetDevice(ls.dev->device()));
+      CU(cudaEventRecord(ls.ev_surf, ls.dev->stream()));
     }
     return ESDG_B200_OK;
   }
   // (2) volume term overlaps the exchange (solver.hpp:259-262)
   for (auto& ls : shards_)
     RC(timed(ls, kClsVolume, [&] {
-      return ls.dev->rhs(kModeVolume, src, dst, a_old, a_new, source, stage, nullptr);
+      return ls.dev->rhs(kModeVolume, src, dst, a_old, a_new, source, stage, ESDG_B200_PART_ALL, nullptr);
     }));
   if (volume_only) return ESDG_B200_OK;
   if (halo) RC(exchange_end());
   // (3)-(5) face fluxes and lift (solver.hpp:264-337)
   for (auto& ls : shards_) {
     RC(timed(ls, kClsSurface, [&] {
-      return ls.dev->rhs(kModeSurface, src, dst, 1.0, a_new, 0, stage, nullptr);
+      return ls.dev->rhs(kModeSurface, src, dst, 1.0, a_new, 0, stage, ESDG_B200_PART_ALL, nullptr);
     }));
     if (halo && !ls.halo.peers.empty()) {
       CU(cudaSetDevice(ls.dev->device()));
@@ -569,18 +594,27 @@ int SolverCore::rhs(int src, int dst, double a_old, double a_new,
 // One LSRK stage in one kernel per partition: k <- a k + dt RHS(q), q <- q + b k
 int SolverCore::stage_fused(double a_old, double a_new, double b, int stage) {
   const bool halo = any_halo_;
-  if (halo) {
-    RC(exchange_begin(ESDG_B200_REG_Q));
-    RC(exchange_end());
-  }
-  for (auto& ls : shards_) {
+  const bool split = halo && overlap_;
+  const int source = opt_.settings.coriolis_mode != 0 ? 1 : 0;
+  if (halo) RC(exchange_begin(ESDG_B200_REG_Q));
+  // groups without a ghost face first: they hide the transfer
+  for (auto& ls : shards_)
     RC(timed(ls, kClsVolume, [&] {
-      return ls.dev->stage_fused(a_old, a_new, b, opt_.settings.coriolis_mode != 0 ? 1 : 0, stage, nullptr);
+      return ls.dev->stage_fused(a_old, a_new, b, source, stage,
+                                 split && !ls.halo.peers.empty() ? ESDG_B200_PART_INTERIOR
+                                                                 : ESDG_B200_PART_ALL,
+                                 nullptr);
     }));
-    if (halo && !ls.halo.peers.empty()) {
-      CU(cudaSetDevice(ls.dev->device()));
-      CU(cudaEventRecord(ls.ev_surf, ls.dev->stream()));
-    }
+  if (halo) RC(exchange_end());
+  for (auto& ls : shards_) {
+    if (!halo || ls.halo.peers.empty()) continue;
+    if (split)
+      RC(timed(ls, kClsVolume, [&] {
+        return ls.dev->stage_fused(a_old, a_new, b, source, stage, ESDG_B200_PART_BOUNDARY,
+                                   nullptr);
+      }));
+    CU(cudaSetDevice(ls.dev->device()));
+    CU(cudaEventRecord(ls.ev_surf, ls.dev->stream()));
   }
   return ESDG_B200_OK;
 }

@@ -47,6 +47,8 @@ public:
   const Mesh& mesh() const { return *mesh_; }
 
   int set_path(int path);
+  void set_overlap(bool on) { overlap_ = on; }
+  void overlap_elements(int64_t* interior, int64_t* total);
   int set_settings(const esdg_b200_settings& s);
   int halo(int32_t* peer, int64_t* offset, int64_t* count, int capacity) const;
   ShardBase* shard(size_t i) { return shards_[i].dev.get(); }
@@ -121,6 +123,7 @@ private:
   int path_ = ESDG_B200_PATH_SPLIT;
   int reduction_ = ESDG_B200_REDUCE_ON_DEVICE;
   bool any_halo_ = false;
+  bool overlap_ = true; // one-pass paths: interior groups hide the exchange
   esdg_b200_error err_{};
   bool timing_ = false;
   std::vector<TimedLaunch> pending_;

@@ -207,6 +207,10 @@ public:
     CU(cudaMemset(k_, 0, state_bytes));
     CU(alloc_copy(&phi_, d.phi, sizeof(Real) * size_t(ne_) * size_t(n3_)));
     CU(alloc_copy(&nbr_, d.nbr, sizeof(int32_t) * size_t(ne_) * 6));
+    {
+      const int rc = build_groups(d.nbr);
+      if (rc != ESDG_B200_OK) return rc;
+    }
     CU(alloc_copy(&ghost_phi_, d.ghost_phi,
                   sizeof(Real) * size_t(n_ghost_) * size_t(n2_)));
     CU(alloc_copy(&send_elem_, d.send_elem, sizeof(int32_t) * size_t(n_send_)));
@@ -295,33 +299,47 @@ public:
   }
 
   int rhs(int mode, int src, int dst, double a_old, double a_new,
-          int with_source, int stage, cudaStream_t st) override {
+          int with_source, int stage, int part, cudaStream_t st) override {
     if ((src != 0 && src != 1) || (dst != 0 && dst != 1) || src == dst)
       return bad("rhs: src and dst must be distinct registers 0/1");
-    return launch(mode, src, dst, a_old, a_new, 0.0, nullptr, with_source, stage, st);
+    if (part < ESDG_B200_PART_ALL || part > ESDG_B200_PART_BOUNDARY) return bad("rhs: bad part");
+    return launch(mode, src, dst, a_old, a_new, 0.0, nullptr, with_source, stage, part, st);
   }
 
   int stage_fused(double a_old, double a_new, double b, int with_source, int stage,
-                  cudaStream_t st) override {
+                  int part, cudaStream_t st) override {
+    if (part < ESDG_B200_PART_ALL || part > ESDG_B200_PART_BOUNDARY)
+      return bad("stage_fused: bad part");
     CU(cudaSetDevice(device_));
     if (!q_alt_) {
       const size_t state_bytes = sizeof(Real) * size_t(ne_) * 5 * size_t(n3_);
       CU(cudaMalloc(&q_alt_, state_bytes + 64));
     }
-    const int rc = launch(kModeFused, 0, 1, a_old, a_new, b, q_alt_, with_source, stage, st);
-    if (rc == ESDG_B200_OK) std::swap(q_, q_alt_); // the new state is current
+    const int rc = launch(kModeFused, 0, 1, a_old, a_new, b, q_alt_, with_source, stage, part, st);
+    // the new state is current once every element has been through the stage
+    if (rc == ESDG_B200_OK && part != ESDG_B200_PART_INTERIOR) std::swap(q_, q_alt_);
     return rc;
   }
 
+  int64_t part_elements(int part) const override {
+    return part == ESDG_B200_PART_ALL        ? ne_
+           : part == ESDG_B200_PART_INTERIOR ? n_part_elems_[0]
+           : part == ESDG_B200_PART_BOUNDARY ? n_part_elems_[1]
+                                             : -1;
+  }
+
   int launch(int mode, int src, int dst, double a_old, double a_new, double b,
-             Real* q_next, int with_source, int stage, cudaStream_t st) {
+             Real* q_next, int with_source, int stage, int part, cudaStream_t st) {
     CU(cudaSetDevice(device_));
+    const int32_t* groups = part == ESDG_B200_PART_ALL ? nullptr : groups_ + (part == ESDG_B200_PART_BOUNDARY ? n_groups_[0] : 0);
+    const long long n_groups = part == ESDG_B200_PART_ALL ? 0 : n_groups_[part - 1];
+    if (part != ESDG_B200_PART_ALL && n_groups == 0) return ESDG_B200_OK;
     cudaError_t e = cudaErrorInvalidValue;
     switch (nq_) {
 #define ESDG_CASE(NQ)                                                          \
   case NQ:                                                                     \
     e = run_rhs<NQ>(mode, src, dst, a_old, a_new, b, q_next, with_source,      \
-                    stage, pick(st));                                          \
+                    stage, groups, n_groups, pick(st));                        \
     break;
       ESDG_CASE(2) ESDG_CASE(3) ESDG_CASE(4) ESDG_CASE(5) ESDG_CASE(6)
       ESDG_CASE(7) ESDG_CASE(8)
@@ -449,8 +467,9 @@ private:
   template <int NQ>
   cudaError_t run_rhs(int mode, int src, int dst, double a_old, double a_new,
                       double b, Real* q_next, int with_source, int stage,
-                      cudaStream_t st) {
+                      const int32_t* groups, long long n_groups, cudaStream_t st) {
     dev::RhsParams<Real, NQ> P;
+    P.groups = groups;
     P.q = reg_ptr(src);
     P.q_next = q_next;
     P.b_upd = Real(b);
@@ -490,7 +509,40 @@ private:
     }
     P.dissipation = dissipation_;
     P.stage = stage;
-    return launch_rhs<Real, NQ>(mode, P, st);
+    return launch_rhs<Real, NQ>(mode, P, n_groups, st);
+  }
+
+  // Element groups (the EPB consecutive elements one CTA of rhs_kernel owns)
+  // sorted into "no ghost face" and "at least one ghost face": the one-pass
+  // kernels run the first list while the traces travel and the second after
+  // they have landed -- the reference's order volume -> wait -> ghost faces
+  // (solver.hpp:259-294) at group granularity.
+  int build_groups(const int32_t* nbr) {
+    int threads = 0, epb = 1;
+    size_t smem = 0;
+    switch (nq_) {
+#define ESDG_CASE(NQ) \
+  case NQ: rhs_launch_shape<Real, NQ>(&threads, &epb, &smem); break;
+      ESDG_CASE(2) ESDG_CASE(3) ESDG_CASE(4) ESDG_CASE(5) ESDG_CASE(6)
+      ESDG_CASE(7) ESDG_CASE(8)
+#undef ESDG_CASE
+      default: return bad("unsupported nq");
+    }
+    const int64_t ng = (ne_ + epb - 1) / epb;
+    std::vector<int32_t> interior, boundary;
+    n_part_elems_[0] = n_part_elems_[1] = 0;
+    for (int64_t g = 0; g < ng; ++g) {
+      const int64_t lo = g * epb, hi = std::min<int64_t>(ne_, lo + epb);
+      bool ghost = false;
+      for (int64_t i = lo * 6; i < hi * 6 && !ghost; ++i) ghost = nbr[i] <= -2;
+      (ghost ? boundary : interior).push_back(int32_t(g));
+      n_part_elems_[ghost ? 1 : 0] += hi - lo;
+    }
+    n_groups_[0] = int64_t(interior.size());
+    n_groups_[1] = int64_t(boundary.size());
+    interior.insert(interior.end(), boundary.begin(), boundary.end());
+    CU(alloc_copy(&groups_, interior.data(), sizeof(int32_t) * interior.size()));
+    return ESDG_B200_OK;
   }
 
   static cudaError_t alloc_copy_impl(void** dst, const void* src, size_t bytes) {
@@ -524,6 +576,7 @@ private:
     cudaFree(k_);
     cudaFree(phi_);
     cudaFree(nbr_);
+    cudaFree(groups_);
     cudaFree(ghost_phi_);
     cudaFree(send_elem_);
     cudaFree(send_face_);
@@ -550,7 +603,8 @@ private:
   Real *q_ = nullptr, *q_alt_ = nullptr, *k_ = nullptr, *phi_ = nullptr, *ghost_phi_ = nullptr;
   Real *recv_ = nullptr, *send_ = nullptr, *cor_f_ = nullptr;
   int32_t *nbr_ = nullptr, *send_elem_ = nullptr, *send_face_ = nullptr,
-          *ylevel_ = nullptr;
+          *ylevel_ = nullptr, *groups_ = nullptr;
+  int64_t n_groups_[2] = {0, 0}, n_part_elems_[2] = {0, 0};
   unsigned long long *flag_ = nullptr, *flag_host_ = nullptr;
   double *red_out_ = nullptr, *red_tab_ = nullptr;
   unsigned* red_bad_ = nullptr;
@@ -839,7 +893,7 @@ int esdg_b200_shard_volume(esdg_b200_shard* s, int src, int dst, double a_old,
   if (!s) return ESDG_B200_BADARG;
   s->last_src = src;
   return s->impl->rhs(esdg_b200::kModeVolume, src, dst, a_old, a_new,
-                      with_source, stage, cudaStream_t(stream));
+                      with_source, stage, ESDG_B200_PART_ALL, cudaStream_t(stream));
 }
 
 int esdg_b200_shard_surface(esdg_b200_shard* s, int src, int dst, double a_new,
@@ -847,7 +901,7 @@ int esdg_b200_shard_surface(esdg_b200_shard* s, int src, int dst, double a_new,
   if (!s) return ESDG_B200_BADARG;
   s->last_src = src;
   return s->impl->rhs(esdg_b200::kModeSurface, src, dst, 1.0, a_new, 0, stage,
-                      cudaStream_t(stream));
+                      ESDG_B200_PART_ALL, cudaStream_t(stream));
 }
 
 int esdg_b200_shard_rhs_fused(esdg_b200_shard* s, int src, int dst,
@@ -856,14 +910,38 @@ int esdg_b200_shard_rhs_fused(esdg_b200_shard* s, int src, int dst,
   if (!s) return ESDG_B200_BADARG;
   s->last_src = src;
   return s->impl->rhs(esdg_b200::kModeFused, src, dst, a_old, a_new, 1, stage,
-                      cudaStream_t(stream));
+                      ESDG_B200_PART_ALL, cudaStream_t(stream));
+}
+
+int esdg_b200_shard_rhs_fused_part(esdg_b200_shard* s, int src, int dst,
+                                   double a_old, double a_new, int stage,
+                                   int part, void* stream) {
+  if (!s) return ESDG_B200_BADARG;
+  s->last_src = src;
+  return s->impl->rhs(esdg_b200::kModeFused, src, dst, a_old, a_new, 1, stage,
+                      part, cudaStream_t(stream));
+}
+
+int esdg_b200_shard_stage_fused_part(esdg_b200_shard* s, double a_old,
+                                     double a_new, double b, int stage,
+                                     int part, void* stream) {
+  if (!s) return ESDG_B200_BADARG;
+  s->last_src = ESDG_B200_REG_Q;
+  return s->impl->stage_fused(a_old, a_new, b, 1, stage, part, cudaStream_t(stream));
+}
+
+int esdg_b200_shard_part_elements(esdg_b200_shard* s, int part, int64_t* count) {
+  if (!s || !count) return ESDG_B200_BADARG;
+  *count = s->impl->part_elements(part);
+  return *count < 0 ? ESDG_B200_BADARG : ESDG_B200_OK;
 }
 
 int esdg_b200_shard_stage_fused(esdg_b200_shard* s, double a_old, double a_new,
                                 double b, int stage, void* stream) {
   if (!s) return ESDG_B200_BADARG;
   s->last_src = ESDG_B200_REG_Q;
-  return s->impl->stage_fused(a_old, a_new, b, 1, stage, cudaStream_t(stream));
+  return s->impl->stage_fused(a_old, a_new, b, 1, stage, ESDG_B200_PART_ALL,
+                              cudaStream_t(stream));
 }
 
 int esdg_b200_shard_axpy(esdg_b200_shard* s, double b, void* stream) {

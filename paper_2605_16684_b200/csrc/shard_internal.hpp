@@ -30,12 +30,15 @@ public:
   virtual int64_t launch_count() const = 0;
   virtual void set_dissipation(int on) = 0;
   virtual int pack(int src, cudaStream_t st) = 0;
-  // mode: RhsMode (esdg_launch.hpp)
+  // mode: RhsMode (esdg_launch.hpp); part: ESDG_B200_PART_* -- all elements,
+  // or only the element groups without / with a ghost face
   virtual int rhs(int mode, int src, int dst, double a_old, double a_new,
-                  int with_source, int stage, cudaStream_t st) = 0;
-  // k <- a_old k + a_new RHS(q); q <- q + b k in one kernel (q double buffered)
+                  int with_source, int stage, int part, cudaStream_t st) = 0;
+  // k <- a_old k + a_new RHS(q); q <- q + b k in one kernel (q double buffered;
+  // the buffers swap after PART_ALL or PART_BOUNDARY)
   virtual int stage_fused(double a_old, double a_new, double b, int with_source,
-                          int stage, cudaStream_t st) = 0;
+                          int stage, int part, cudaStream_t st) = 0;
+  virtual int64_t part_elements(int part) const = 0;
   virtual int axpy(double b, cudaStream_t st) = 0;
   virtual int check(cudaStream_t st, int src, esdg_b200_error* err) = 0;
   // K6: one partial per element, see esdg_b200_shard_reduce

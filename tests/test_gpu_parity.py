@@ -179,6 +179,38 @@ def test_partition_bitwise_trajectory(port, ranks, path):
     assert np.array_equal(states[0], states[1])
 
 
+@pytest.mark.parametrize("path", [capi.PATH_FUSED, capi.PATH_STAGE])
+@pytest.mark.parametrize("ranks,order", [(2, 3), (3, 4), (5, 2)])
+def test_one_pass_overlap_bitwise(port, ranks, order, path):
+    """The one-pass kernels run the element groups without a ghost face while
+    the traces travel and the other groups afterwards (rhs_job's order,
+    solver.hpp:259-294). That split, the wait-first single launch and the
+    single-partition solver agree bitwise; with two or three partitions of a
+    512-element mesh the interior part is neither empty nor everything."""
+    states = []
+    for r, overlap in ((1, True), (ranks, True), (ranks, False)):
+        o, g = make(port, "bubble", (3, False), order, ranks=r, path=path)
+        g.set_overlap(overlap)
+        interior, total = g.overlap_elements()
+        assert total == 512
+        if r == 1:
+            assert interior == total
+        else:
+            # five partitions of 102 elements in groups of 14 (order 2): every
+            # group touches a partition boundary -- the all-boundary edge case
+            assert (0 < interior < total) if ranks < 5 else (0 <= interior < total)
+        q = o.init_case(po.CASE_BUBBLE_SHARP).copy()
+        g.set_state(q)
+        dt = o.compute_dt(0.5)
+        for _ in range(3):
+            g.step(dt)
+        rhs = g.assemble_rhs(g.get_state())
+        states.append((g.get_state(), rhs))
+    for a in states[1:]:
+        assert np.array_equal(states[0][0], a[0])
+        assert np.array_equal(states[0][1], a[1])
+
+
 @pytest.mark.parametrize("path", [capi.PATH_SPLIT, capi.PATH_FUSED, capi.PATH_STAGE])
 def test_trajectory_config1(port, path):
     """BASELINE.json configs[0]: 10 RK steps of the sharp bubble, N=4, 8^3.
