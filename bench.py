@@ -235,7 +235,7 @@ def main_b200(args, rank, local_rank, world):
         base = tuple(args.base) if args.base else (12, 2 * world, 1)
         cfg = capi.channel_mesh_config(args.refinement, base)
         settings = capi.Settings(1, 2, 1e-4, 1.6e-11, 3e6)
-        case_id = capi.CASE_BAROCLINIC
+        case_id = capi.CASE_BAROCLINIC_JET
     mesh = capi.Mesh(cfg)
 
     if world > 1:

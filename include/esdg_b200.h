@@ -298,7 +298,15 @@ enum {
   ESDG_B200_CASE_HYDROSTATIC = 2,   /* cases.hpp:18-38 */
   ESDG_B200_CASE_ENTROPY_TEST = 3,  /* cases.hpp:120-156, iparam = seed */
   ESDG_B200_CASE_CONSTANT = 4,      /* test_helpers.hpp:41-52 */
-  ESDG_B200_CASE_BAROCLINIC = 5     /* ours; the reference ships none */
+  ESDG_B200_CASE_BAROCLINIC = 5,    /* ours; the reference ships none */
+  /* Balanced zonal jet in a beta-plane channel after Ullrich, Reed and
+   * Jablonowski (2015), the test PAPER.md:465-472 runs: geostrophic and
+   * hydrostatic balance in pressure coordinates against the Coriolis
+   * parameter of the solver's own settings (f0, beta, y0), plus a Gaussian
+   * zonal-wind perturbation. dparam = {u0, u_pert, T0, lapse rate, b}; zeros
+   * select 35 m/s, 1 m/s, 288 K, 0.005 K/m, 2; u_pert < 0: none. Ours as well (runner.cpp:70-74
+   * has no channel state); the balance is what the tests check. */
+  ESDG_B200_CASE_BAROCLINIC_JET = 6
 };
 
 enum {
@@ -365,6 +373,14 @@ int64_t esdg_b200_solver_n_ghost(const esdg_b200_solver* s);
  * only when keep_host != 0. dparam: case parameters (may be NULL). */
 int esdg_b200_solver_init_case(esdg_b200_solver* s, int case_id,
                                uint64_t iparam, const double* dparam);
+/* The same generators at one point, host only (no device needed): q[5] at
+ * (x, y, z) with phi = gravity * z. settings may be NULL (no Coriolis).
+ * Returns ESDG_B200_BADARG when the generator leaves its domain. */
+int esdg_b200_case_point(int case_id, const esdg_b200_mesh_config* mesh,
+                         const esdg_b200_gas* gas,
+                         const esdg_b200_settings* settings, uint64_t iparam,
+                         const double* dparam, double x, double y, double z,
+                         double q[5]);
 /* state()/k register as host StateField arrays of the LOCAL element range */
 int esdg_b200_solver_set_state(esdg_b200_solver* s, int reg, const void* host);
 int esdg_b200_solver_get_state(esdg_b200_solver* s, int reg, void* host);

@@ -22,7 +22,7 @@ REG_Q, REG_K = 0, 1
 PATH_SPLIT, PATH_FUSED, PATH_STAGE = 0, 1, 2
 REDUCE_ON_DEVICE, REDUCE_ON_HOST = 0, 1
 (CASE_BUBBLE_SHARP, CASE_BUBBLE_SMOOTH, CASE_HYDROSTATIC, CASE_ENTROPY_TEST,
- CASE_CONSTANT, CASE_BAROCLINIC) = range(6)
+ CASE_CONSTANT, CASE_BAROCLINIC, CASE_BAROCLINIC_JET) = range(7)
 
 
 class MeshConfig(C.Structure):
@@ -134,6 +134,7 @@ SIGNATURES = {
     "esdg_b200_solver_recv_ptr": (_vp, [_vp]),
     "esdg_b200_solver_n_ghost": (_i64, [_vp]),
     "esdg_b200_solver_init_case": (_i, [_vp, _i, C.c_uint64, _dp]),
+    "esdg_b200_case_point": (_i, [_i, _vp, _vp, _vp, C.c_uint64, _dp, _d, _d, _d, _dp]),
     "esdg_b200_solver_set_state": (_i, [_vp, _i, _vp]),
     "esdg_b200_solver_get_state": (_i, [_vp, _i, _vp]),
     "esdg_b200_solver_swap_state": (_i, [_vp, _i, _vp, _vp]),
@@ -232,6 +233,19 @@ def bubble_mesh_config(refinement, periodic_z=False, base=(1, 1, 1), scale=(1, 1
 def channel_mesh_config(refinement, base=(12, 2, 1)) -> MeshConfig:
     """case_defaults(BaroclinicChannel), core/src/config.cpp:84-95."""
     return mesh_config(base, refinement, (0., 0., 0.), (4e7, 6e6, 3e4), (0, 1, 1))
+
+
+def case_point(case_id, cfg: MeshConfig, gas: "Gas", settings: "Settings | None", x, y, z,
+               iparam=0, dparam=None):
+    """The named initial state at one point (host only), as five doubles."""
+    d = np.zeros(8)
+    if dparam is not None:
+        d[:len(dparam)] = dparam
+    q = np.zeros(5)
+    check(lib().esdg_b200_case_point(case_id, C.byref(cfg), C.byref(gas),
+                                      C.byref(settings) if settings is not None else None,
+                                      iparam, d.ctypes.data_as(_dp), x, y, z, q.ctypes.data_as(_dp)))
+    return q
 
 
 class Mesh:

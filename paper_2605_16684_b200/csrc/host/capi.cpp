@@ -252,6 +252,30 @@ int64_t esdg_b200_solver_n_ghost(const esdg_b200_solver* s) {
   return (s && s->core->n_shards() == 1) ? s->core->shard(0)->n_ghost() : 0;
 }
 
+int esdg_b200_case_point(int case_id, const esdg_b200_mesh_config* mesh,
+                         const esdg_b200_gas* gas, const esdg_b200_settings* settings,
+                         uint64_t iparam, const double* dparam, double x, double y, double z,
+                         double q[5]) {
+  if (!mesh || !gas || !q) return ESDG_B200_BADARG;
+  esdg_b200::host::CaseEval ce;
+  ce.case_id = case_id;
+  ce.gas = *gas;
+  ce.mesh = *mesh;
+  if (settings) ce.settings = *settings;
+  ce.iparam = iparam;
+  if (dparam)
+    for (int i = 0; i < 5; ++i) ce.dparam[i] = dparam[i];
+  if (!ce.prepare()) {
+    esdg_b200::set_message("case_point: unknown case");
+    return ESDG_B200_BADARG;
+  }
+  if (!ce.point(x, y, z, gas->gravity * z, q)) {
+    esdg_b200::set_message("case_point: state generator left its domain");
+    return ESDG_B200_BADARG;
+  }
+  return ESDG_B200_OK;
+}
+
 int esdg_b200_solver_init_case(esdg_b200_solver* s, int case_id, uint64_t iparam,
                                const double* dparam) {
   CORE(s);

@@ -6,7 +6,10 @@
 // The baroclinic-channel state is OURS: the reference ships the channel mesh
 // and beta-plane defaults (core/src/config.cpp:84-95) but no initial state
 // (core/src/runner.cpp:70-74), so its IC is "parity unpinned" by definition;
-// the RHS on it is still checked against the oracle.
+// the RHS on it is still checked against the oracle. CASE_BAROCLINIC_JET is
+// the balanced jet of Ullrich, Reed & Jablonowski (2015), which PAPER.md:465-472
+// runs; it is derived below from the two balances it satisfies, and those are
+// what tests/test_host_mirror.py::test_baroclinic_jet_is_balanced checks.
 #include <cmath>
 
 #include "host_types.hpp"
@@ -29,7 +32,7 @@ double unit(uint64_t& state) {
 } // namespace
 
 bool CaseEval::prepare() {
-  if (case_id < 0 || case_id > ESDG_B200_CASE_BAROCLINIC) return false;
+  if (case_id < 0 || case_id > ESDG_B200_CASE_BAROCLINIC_JET) return false;
   if (case_id == ESDG_B200_CASE_ENTROPY_TEST) {
     // five seeded 3-mode Fourier fields: rho, p, u1, u2, u3 (cases.hpp:86-134)
     uint64_t s = iparam;
@@ -126,6 +129,73 @@ bool CaseEval::point(double x, double y, double z, double phi, double q[5]) cons
       const double Lp = 0.1 * Ly;
       const double r2 = ((x - xc) * (x - xc) + (y - yc) * (y - yc)) / (Lp * Lp);
       const double u1 = U0 * sy * sy * (z - mesh.lo[2]) / Lz + up * std::exp(-r2);
+      q[0] = rho;
+      q[1] = rho * u1;
+      q[2] = 0.0;
+      q[3] = 0.0;
+      q[4] = p / (gas.gamma - 1.0) + 0.5 * rho * u1 * u1 + rho * phi;
+      return true;
+    }
+    case ESDG_B200_CASE_BAROCLINIC_JET: {
+      // Pressure coordinate eta = p / p0, s = ln eta, F(s) = s exp(-(s/b)^2).
+      //   u(y, eta)   = -u0 sin^2(pi yy / Ly) F(s)              yy = y - lo_y
+      //   Phi(y, eta) = Phibar(eta) + Phi'(yy) F(s)
+      //   T(y, eta)   = Tbar(eta) + Phi'(yy) / R (2 s^2 / b^2 - 1) exp(-(s/b)^2)
+      // Hydrostatic balance dPhi/ds = -R T fixes T from Phi; with the lapse-rate
+      // column Tbar = T0 eta^(R Gamma / g), Phibar = T0 g / Gamma (1 - eta^(R Gamma / g)).
+      // Geostrophic balance f u = -dPhi/dy at constant eta, f = fa + beta yy,
+      // fixes dPhi'/dyy = u0 f sin^2(pi yy / Ly); Phi' is its integral with zero
+      // mean over the channel width. The Coriolis parameter is the solver's
+      // (CoriolisParams::f_at, physics.hpp:276-295), so the state is steady
+      // under the source term the RHS actually applies.
+      const double u0 = dparam[0] != 0.0 ? dparam[0] : 35.0;
+      const double up = dparam[1] < 0.0 ? 0.0 : (dparam[1] != 0.0 ? dparam[1] : 1.0);
+      const double T0 = dparam[2] != 0.0 ? dparam[2] : 288.0;
+      const double lapse = dparam[3] != 0.0 ? dparam[3] : 0.005;
+      const double b = dparam[4] != 0.0 ? dparam[4] : 2.0;
+      const double g = gas.gravity, R = gas.R;
+      if (!(g > 0.0)) return false;
+      const double Lx = mesh.hi[0] - mesh.lo[0], Ly = mesh.hi[1] - mesh.lo[1];
+      const double yy = y - mesh.lo[1];
+      double fa = 0.0, beta = 0.0;
+      if (settings.coriolis_mode == 1) fa = settings.f0;
+      if (settings.coriolis_mode == 2) {
+        beta = settings.beta;
+        fa = settings.f0 + beta * (mesh.lo[1] - settings.y0);
+      }
+      const double w = 2.0 * M_PI * yy / Ly, sw = std::sin(w), cw = std::cos(w);
+      const double ip = Ly / M_PI; // Ly / pi
+      const double dphi =
+          0.5 * u0 *
+          (fa * (yy - 0.5 * Ly - 0.5 * ip * sw) +
+           0.5 * beta * (yy * yy - ip * yy * sw - 0.5 * ip * ip * cw - Ly * Ly / 3.0 - 0.5 * ip * ip));
+      const double kappa = R * lapse / g;
+      // Newton iteration on s: Phi(s) = g z, dPhi/ds = -R T(s)
+      double s = -g * z / (R * T0), T = T0, F = 0.0;
+      for (int it = 0; it < 60; ++it) {
+        const double e = std::exp(-(s / b) * (s / b));
+        F = s * e;
+        const double ek = std::exp(kappa * s); // eta^kappa
+        T = T0 * ek + dphi / R * (2.0 * s * s / (b * b) - 1.0) * e;
+        if (!(T > 0.0)) return false;
+        const double Phi = T0 * g / lapse * (1.0 - ek) + dphi * F;
+        const double ds = (Phi - g * z) / (R * T);
+        s += ds;
+        if (std::abs(ds) <= 1e-15 * (1.0 + std::abs(s))) break;
+      }
+      {
+        const double e = std::exp(-(s / b) * (s / b));
+        F = s * e;
+        T = T0 * std::exp(kappa * s) + dphi / R * (2.0 * s * s / (b * b) - 1.0) * e;
+      }
+      const double p = gas.p0 * std::exp(s);
+      const double rho = p / (R * T);
+      const double sy = std::sin(M_PI * yy / Ly);
+      // perturbation centre and width: 2000 km, 2500 km, 600 km in the
+      // 40000 km x 6000 km channel, scaled with the box
+      const double xc = mesh.lo[0] + 0.05 * Lx, yc = mesh.lo[1] + 2.5 / 6.0 * Ly, Lp = 0.1 * Ly;
+      const double r2 = ((x - xc) * (x - xc) + (y - yc) * (y - yc)) / (Lp * Lp);
+      const double u1 = -u0 * sy * sy * F + up * std::exp(-r2);
       q[0] = rho;
       q[1] = rho * u1;
       q[2] = 0.0;

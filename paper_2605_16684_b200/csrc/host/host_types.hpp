@@ -87,6 +87,7 @@ struct CaseEval {
   int case_id = 0;
   esdg_b200_gas gas{};
   esdg_b200_mesh_config mesh{};
+  esdg_b200_settings settings{}; // the balanced jet reads the Coriolis parameter
   uint64_t iparam = 0;
   double dparam[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   // entropy-test Fourier fields

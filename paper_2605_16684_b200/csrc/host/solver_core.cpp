@@ -381,6 +381,7 @@ int SolverCore::init_case(int case_id, uint64_t iparam, const double* dparam) {
   ce.case_id = case_id;
   ce.gas = opt_.gas;
   ce.mesh = mesh_->cfg;
+  ce.settings = opt_.settings;
   ce.iparam = iparam;
   if (dparam)
     for (int i = 0; i < 5; ++i) ce.dparam[i] = dparam[i];

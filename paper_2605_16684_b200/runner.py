@@ -46,7 +46,7 @@ def run_case(case="bubble", order=4, refinement=3, base=None, precision="f64", c
         settings, case_id = capi.Settings(1, 0, 0.0, 0.0, 0.0), capi.CASE_BUBBLE_SHARP
     elif case == "baroclinic":
         cfg = capi.channel_mesh_config(refinement, tuple(base or (12, 2, 1)))
-        settings, case_id = capi.Settings(1, 2, 1e-4, 1.6e-11, 3e6), capi.CASE_BAROCLINIC
+        settings, case_id = capi.Settings(1, 2, 1e-4, 1.6e-11, 3e6), capi.CASE_BAROCLINIC_JET
     else:
         raise ValueError(f"unknown case {case!r}")
     mesh = capi.Mesh(cfg)

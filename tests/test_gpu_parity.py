@@ -346,6 +346,36 @@ def test_baroclinic_channel_rhs_and_steps(port, path):
     assert float(np.abs(gs[:, 1:4] - o.state[:, 1:4]).max()) <= 1e-11 * mom
 
 
+def test_baroclinic_jet_discrete_balance(port):
+    """CASE_BAROCLINIC_JET (the balanced jet PAPER.md:465-472 runs, generator
+    ours) without its perturbation is a steady state up to discretisation
+    error: the RHS on it matches the oracle's to TOL64, mass, zonal-momentum and
+    energy tendencies vanish to rounding, and the meridional / vertical
+    momentum tendencies are small against the terms that balance (rho f u ~
+    4e-3, rho g ~ 12 N/m^3) and shrink ~16x per refinement (measured 3.6e-6 ->
+    2.6e-7 and 3.1e-2 -> 1.7e-3). 20 steps leave v, w below 5 cm/s (jet: 30 m/s)."""
+    cor = (2, 1e-4, 1.6e-11, 3e6)
+    res = []
+    for level in (1, 2):
+        margs = ((12, 2, 1), level, (0., 0., 0.), (4e7, 6e6, 3e4), (0, 1, 1))
+        o, g = make(port, "raw", margs, 4, cor=cor, path=capi.PATH_STAGE)
+        g.init_case(capi.CASE_BAROCLINIC_JET, dparam=[0., -1., 0., 0., 0.])
+        q = g.get_state()
+        assert 25.0 < float(np.abs(q[:, 1] / q[:, 0]).max()) < 30.1   # u0 sqrt(2) exp(-1/2) = 30.02
+        want, got = o.assemble_rhs(q.copy()), g.assemble_rhs(q)
+        assert scaled_error(got, want, o.flux_scale(q.copy()) + 1e-4 * np.abs(q).max(axis=(0, 2))) <= TOL64
+        mx = [float(np.abs(got[:, v]).max()) for v in range(5)]
+        assert mx[0] <= 1e-17 and mx[1] <= 1e-13 and mx[4] <= 1e-11, mx
+        res.append(mx)
+    assert res[0][2] <= 1e-5 and res[1][2] <= res[0][2] / 8
+    assert res[0][3] <= 5e-2 and res[1][3] <= res[0][3] / 8
+    dt = g.compute_dt(0.5)
+    for _ in range(20):
+        g.step(dt)
+    q2 = g.get_state()
+    assert float(np.abs(q2[:, 2:4] / q2[:, :1]).max()) <= 5e-2   # measured 1.2e-2, thin air at the lid
+
+
 def test_init_case_matches_oracle(port):
     for case, seed in ((po.CASE_BUBBLE_SHARP, 0), (po.CASE_BUBBLE_SMOOTH, 0), (po.CASE_HYDROSTATIC, 0),
                        (po.CASE_ENTROPY_TEST, 77)):

@@ -151,3 +151,50 @@ def test_rank_halo_consistency(port, idx, world):
                 theirs = face_of[hp["begin"] + hp["send_elem"][poff[0] + i], hp["send_face"][poff[0] + i]]
                 assert mine == theirs
                 assert h["send_face"][off + i] == hp["send_face"][poff[0] + i] ^ 1
+
+
+def _primitives(q, gas, z):
+    rho = q[0]
+    u = q[1:4] / rho
+    p = (gas.gamma - 1.0) * (q[4] - 0.5 * rho * float(u @ u) - rho * gas.gravity * z)
+    return rho, u, p
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_baroclinic_jet_is_balanced(mode):
+    """CASE_BAROCLINIC_JET (ours; Ullrich et al. 2015 as PAPER.md:465-472 runs
+    it) is a steady state of the equations the RHS integrates: with v = w = 0
+    and no x dependence that is hydrostatic balance dp/dz = -rho g and
+    geostrophic balance dp/dy = -rho f u with the solver's own Coriolis
+    parameter f = f0 + beta (y - y0) (physics.hpp:276-306). Checked pointwise
+    with centred differences of the generator's pressure (host only)."""
+    cfg = capi.channel_mesh_config(3)
+    gas = capi.Gas(1.4, 287.0, 1e5, 9.81)
+    st = capi.Settings(1, mode, 1e-4, 1.6e-11, 3e6)
+    nopert = [0.0, -1.0, 0.0, 0.0, 0.0]
+
+    def prim(x, y, z):
+        return _primitives(capi.case_point(capi.CASE_BAROCLINIC_JET, cfg, gas, st, x, y, z, dparam=nopert), gas, z)
+
+    rng = np.random.default_rng(5)
+    umax = 0.0
+    for _ in range(200):
+        x, y, z = rng.uniform(0, 4e7), rng.uniform(2e5, 5.8e6), rng.uniform(50.0, 2.9e4)
+        rho, u, p = prim(x, y, z)
+        assert rho > 0 and p > 0 and u[1] == 0 and u[2] == 0
+        umax = max(umax, abs(u[0]))
+        f = 0.0 if mode == 0 else (1e-4 if mode == 1 else 1e-4 + 1.6e-11 * (y - 3e6))
+        hz, hy = 1.0, 2e3      # truncation h^2 p''' / 6 is 2e-9 resp. 1e-12 relative
+        dpdz = (prim(x, y, z + hz)[2] - prim(x, y, z - hz)[2]) / (2 * hz)
+        dpdy = (prim(x, y + hy, z)[2] - prim(x, y - hy, z)[2]) / (2 * hy)
+        assert abs(dpdz + rho * gas.gravity) <= 1e-7 * rho * gas.gravity
+        # 1e-6 of the largest geostrophic term in the channel (rho f u ~ 4e-3 Pa/m)
+        assert abs(dpdy + rho * f * u[0]) <= 1e-6 * 1.2 * 1.3e-4 * 35.0 + 1e-9
+    assert 25.0 < umax < 36.0
+    # the walls carry no jet, the surface is the p0 surface
+    assert abs(prim(1e6, 0.0, 1.5e4)[1][0]) < 1e-12 and abs(prim(1e6, 6e6, 1.5e4)[1][0]) < 1e-10
+    assert abs(prim(1e6, 2e6, 0.0)[2] - gas.p0) <= 1e-9 * gas.p0
+    # the perturbation: 1 m/s of zonal wind at (2000 km, 2500 km)
+    q0 = capi.case_point(capi.CASE_BAROCLINIC_JET, cfg, gas, st, 2e6, 2.5e6, 1e4, dparam=nopert)
+    q1 = capi.case_point(capi.CASE_BAROCLINIC_JET, cfg, gas, st, 2e6, 2.5e6, 1e4)
+    assert abs((q1[1] - q0[1]) / q0[0] - 1.0) < 1e-12 and q1[0] == q0[0]
