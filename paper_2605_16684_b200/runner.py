@@ -24,6 +24,8 @@ import argparse
 import os
 import time
 
+import numpy as np
+
 from . import capi
 
 
@@ -37,10 +39,48 @@ def work_model(nq: int, bytes_per_real: int) -> dict:
     }
 
 
+def theta_slice(solver, mesh, gas, order):
+    """write_theta_slice (runner.cpp:78-123): potential temperature on the node
+    plane closest to y = 0 (or to the mid-plane when 0 lies outside the box),
+    rows (x, z, theta) sorted by (z, x). Evaluated on the host in 64-bit from
+    the downloaded state, like the reference."""
+    cfg, nq = mesh.cfg, order + 1
+    lo, hi = np.array(cfg.lo[:]), np.array(cfg.hi[:])
+    cells = np.array(cfg.base[:], np.int64) << cfg.refinement
+    delta = (hi - lo) / cells
+    ycut = 0.0 if lo[1] <= 0.0 < hi[1] else 0.5 * (lo[1] + hi[1])
+    lat = mesh.lattice
+    y_lo = lo[1] + lat[:, 1] * delta[1]
+    cut = np.nonzero((y_lo <= ycut) & (ycut < y_lo + delta[1]))[0]
+    xi = capi.reference_element(order)[0]
+
+    def coord(e, d, r):   # mesh.hpp:73-77
+        return lo[d] + (lat[e, d][:, None] + 0.5 * (r[None, :] + 1.0)) * delta[d]
+
+    yn = coord(cut, 1, xi)                                   # [cut, nq]
+    b_best = np.abs(yn - ycut).argmin(axis=1)                # first minimum, like the reference
+    q = solver.get_state().astype(np.float64)[cut].reshape(len(cut), 5, nq, nq, nq)   # [e, v, c, b, a]
+    ph = solver.get_phi().astype(np.float64)[cut].reshape(len(cut), nq, nq, nq)
+    idx = np.arange(len(cut))
+    qs, phs = q[idx, :, :, b_best, :], ph[idx, :, b_best, :]  # [e, v, c, a], [e, c, a]
+    rho = qs[:, 0]
+    ke = 0.5 * (qs[:, 1] ** 2 + qs[:, 2] ** 2 + qs[:, 3] ** 2) / rho
+    p = (gas.gamma - 1.0) * (qs[:, 4] - ke - rho * phs)
+    temp = p / (rho * gas.R)
+    cp = gas.gamma * gas.R / (gas.gamma - 1.0)
+    theta = temp * (gas.p0 / p) ** (gas.R / cp)
+    x = np.broadcast_to(coord(cut, 0, xi)[:, None, :], theta.shape)
+    z = np.broadcast_to(coord(cut, 2, xi)[:, :, None], theta.shape)
+    rows = np.stack([x.ravel(), z.ravel(), theta.ravel()], axis=1)
+    return rows[np.lexsort((rows[:, 2], rows[:, 0], rows[:, 1]))]
+
+
 def run_case(case="bubble", order=4, refinement=3, base=None, precision="f64", courant=0.5,
              steps=100, output_cadence=10, out_dir="run_out", path=capi.PATH_SPLIT,
-             peak_gflops=None, peak_gbps=None, device=0) -> dict:
+             peak_gflops=None, peak_gbps=None, device=0, slices=True) -> dict:
     os.makedirs(out_dir, exist_ok=True)
+    if slices:
+        os.makedirs(os.path.join(out_dir, "slices"), exist_ok=True)
     if case == "bubble":
         cfg = capi.bubble_mesh_config(refinement, False, tuple(base or (1, 1, 1)))
         settings, case_id = capi.Settings(1, 0, 0.0, 0.0, 0.0), capi.CASE_BUBBLE_SHARP
@@ -65,6 +105,11 @@ def run_case(case="bubble", order=4, refinement=3, base=None, precision="f64", c
         prod = solver.entropy_production()
         samples.append((step, t, mass, energy))
         entropy_rows.append((step, t, eta, prod))
+        if slices:
+            with open(os.path.join(out_dir, "slices", f"theta_y0_{step}.csv"), "w") as f:
+                f.write("x,z,theta\n")
+                for r in theta_slice(solver, mesh, solver.gas, order):
+                    f.write(",".join(f"{v:.{digits}g}" for v in r) + "\n")
 
     status, t = "ok", 0.0
     secs = {"volume": 0.0, "surface": 0.0, "update": 0.0}

@@ -476,6 +476,17 @@ def test_runner_outputs(tmp_path):
     assert res["mass_drift"] <= 1e-14 and res["energy_drift"] <= 1e-14
     assert all(row[3] <= 0.0 for row in res["entropy"])
     assert "# status = ok" in (tmp_path / "manifest.txt").read_text()
+    # theta slices (runner.cpp:78-123): one file per sample; at t = 0 the
+    # sharp bubble is 300 K outside and 300.5 K inside (cases.hpp:43-69)
+    files = sorted(p.name for p in (tmp_path / "slices").iterdir())
+    assert files == sorted(f"theta_y0_{s}.csv" for s in (0, 4, 8, 12))
+    rows = np.loadtxt(tmp_path / "slices" / "theta_y0_0.csv", delimiter=",", skiprows=1)
+    assert rows.shape == (4 * 4 * 16, 3)              # 4 x 4 cut elements, 4 x 4 nodes each
+    assert np.array_equal(rows[:, [1, 0]], np.array(sorted(map(tuple, rows[:, [1, 0]]))))
+    th = rows[:, 2]
+    assert np.all((np.abs(th - 300.0) < 1e-9) | (np.abs(th - 300.5) < 1e-9))
+    inside = np.hypot(rows[:, 0], rows[:, 1] - 260.0) <= 250.0
+    assert inside.any() and np.all(np.abs(th[inside] - 300.5) < 1e-9)
 
 
 def test_swap_state_equals_get_then_set(port):
