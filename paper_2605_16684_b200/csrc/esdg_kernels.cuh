@@ -383,16 +383,55 @@ __device__ __forceinline__ void sweep_line(const RhsParams<Real, NQ>& P,
     }
   }
 #ifdef ESDG_LADDER_NO_SYMMETRY
-  // Ladder rung without pair symmetry (the reference's "logmean" variant,
-  // kernels.hpp:27-34): every ORDERED pair is evaluated and only node i is
-  // updated. Build-time switch for the measurement in profiles/; the product
-  // always uses the symmetric sweep below.
+  // Ladder rungs below the product (the reference's optimisation ladder,
+  // kernels.hpp:20-34, ladder.hpp:28-82), build-time switches for the
+  // measurement in profiles/r1_ladder.txt; the product always uses the
+  // symmetric sweep below.
+  //   ESDG_LADDER_NO_SYMMETRY  every ORDERED pair is evaluated and only node i
+  //                            is updated (the "precompute"/"logmean" rungs)
+  //   + ESDG_LADDER_RECOMPUTE  primitives and both logarithms are worked out
+  //                            again inside every flux evaluation, for both
+  //                            nodes (the "baseline"/"fused" rungs:
+  //                            compute_node_vals per evaluation, 2 div + 2 log)
+  //   ESDG_LADDER_IEEE_DIV     (esdg_device.cuh) library division instead of
+  //                            the seed + one cubic step reciprocal
+#ifdef ESDG_LADDER_RECOMPUTE
+  extern __shared__ __align__(16) unsigned char ladder_smem[];
+  const Real* ladder_tab = reinterpret_cast<const Real*>(
+      ladder_smem + SmemMap<Real, NQ, Tile<NQ, sizeof(Real)>::EPB>::kTab);
+  auto again = [&](const Node<Real>& n, Real tie) {
+    // conservative variables back from the parked quantities, then
+    // compute_node_vals (physics.hpp:56-80) once more. The exact zero times
+    // a value of the partner (`tie`, a different one in the two roles) binds
+    // the recomputation to this evaluation; the compiler would otherwise
+    // merge the recomputations of one node.
+    const Real rho = fma_(Real(0), tie, n.hr + n.hr);
+    const Real m1 = rho * n.hun, m2 = rho * n.hut1, m3 = rho * n.hut2; // momenta / 2
+    const Real p = rho * n.hib;                                          // rho / (2 b)
+    const Real inv = rcp_(rho);
+    Node<Real> r;
+    r.hr = Real(0.5) * rho;
+    r.hun = m1 * inv;
+    r.hut1 = m2 * inv;
+    r.hut2 = m3 * inv;
+    r.b = rho * rcp_(p + p);
+    r.hib = p * inv;
+    r.hlr = Real(0.5) * log_(rho, ladder_tab);
+    r.lb = log_(r.b, ladder_tab);
+    r.hphi = n.hphi;
+    return r;
+  };
+#endif
 #pragma unroll
   for (int i = 0; i < NQ; ++i) {
 #pragma unroll
     for (int j = 0; j < NQ; ++j) {
       if (j == i) continue;
+#ifdef ESDG_LADDER_RECOMPUTE
+      const PairFlux<Real> pf = pair_flux(again(nd[i], nd[j].hphi), again(nd[j], nd[i].hun), P.gas.cg);
+#else
       const PairFlux<Real> pf = pair_flux(nd[i], nd[j], P.gas.cg);
+#endif
       const Real cij = P.negd[i * NQ + j];
       const Real fni = fma_(pf.tg, nd[i].hib, pf.f[1]);
       acc[i][0] = fma_(cij, pf.f[0], acc[i][0]);
