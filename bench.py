@@ -462,6 +462,9 @@ def main_b200(args, rank, local_rank, world):
     }
     if exchange is not None:
         line["config"]["halo_exchanges"] = halo_exchanges
+        interior, local = solver.overlap_elements()
+        # elements of rank 0 whose one-pass kernel runs while the traces travel
+        line["config"]["halo_overlap"] = {"interior_elements": interior, "local_elements": local}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
