@@ -198,3 +198,13 @@ def test_baroclinic_jet_is_balanced(mode):
     q0 = capi.case_point(capi.CASE_BAROCLINIC_JET, cfg, gas, st, 2e6, 2.5e6, 1e4, dparam=nopert)
     q1 = capi.case_point(capi.CASE_BAROCLINIC_JET, cfg, gas, st, 2e6, 2.5e6, 1e4)
     assert abs((q1[1] - q0[1]) / q0[0] - 1.0) < 1e-12 and q1[0] == q0[0]
+
+
+def test_library_is_a_product_build():
+    """The ladder rungs and tuning hooks are compile-time switches (make
+    EXTRA=-DESDG_LADDER_... / -DESDG_TUNE_...); the library the tests, smoke()
+    and bench.py load must not carry any of them. The Makefile records the
+    flags of the last build and rebuilds everything when they change."""
+    flags = open(os.path.join(capi.CSRC, "build", ".flags")).read()
+    assert "ESDG_LADDER" not in flags and "ESDG_TUNE" not in flags, flags
+    assert "arch=compute_100a,code=sm_100a" in flags and "-lineinfo" in flags
