@@ -229,16 +229,31 @@ template <> struct Tile<4, 8> { static constexpr int EPB = 8, MINB = 3; static c
 #define ESDG_TUNE_MINB 3
 #endif
 template <> struct Tile<5, 8> { static constexpr int EPB = ESDG_TUNE_EPB, MINB = ESDG_TUNE_MINB; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
-template <> struct Tile<6, 8> { static constexpr int EPB = 3, MINB = 2; static constexpr int FPI = 2; static constexpr bool LEAN = false; };
-template <> struct Tile<7, 8> { static constexpr int EPB = 2, MINB = 2; static constexpr int FPI = 2; static constexpr bool LEAN = true; };
+#ifndef ESDG_TUNE_T68E
+#define ESDG_TUNE_T68E 3
+#define ESDG_TUNE_T68M 2
+#define ESDG_TUNE_T78E 2
+#define ESDG_TUNE_T78M 2
+#define ESDG_TUNE_T64E 3
+#define ESDG_TUNE_T64M 4
+#define ESDG_TUNE_T74E 5
+#define ESDG_TUNE_T74M 2
+#endif
+#ifndef ESDG_TUNE_T84E
+#define ESDG_TUNE_T84E 2
+#define ESDG_TUNE_T84M 3
+#endif
+template <int E, int M> struct TilePick { static constexpr int EPB = E, MINB = M; };
+template <> struct Tile<6, 8> : TilePick<ESDG_TUNE_T68E, ESDG_TUNE_T68M> { static constexpr int FPI = 2; static constexpr bool LEAN = false; };
+template <> struct Tile<7, 8> : TilePick<ESDG_TUNE_T78E, ESDG_TUNE_T78M> { static constexpr int FPI = 2; static constexpr bool LEAN = true; };
 template <> struct Tile<8, 8> { static constexpr int EPB = 1, MINB = 3; static constexpr int FPI = 2; static constexpr bool LEAN = true; };
 template <> struct Tile<2, 4> { static constexpr int EPB = 32, MINB = 4; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
 template <> struct Tile<3, 4> { static constexpr int EPB = 14, MINB = 4; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
 template <> struct Tile<4, 4> { static constexpr int EPB = 8, MINB = 4; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
 template <> struct Tile<5, 4> { static constexpr int EPB = 5, MINB = 5; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
-template <> struct Tile<6, 4> { static constexpr int EPB = 3, MINB = 4; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
-template <> struct Tile<7, 4> { static constexpr int EPB = 2, MINB = 4; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
-template <> struct Tile<8, 4> { static constexpr int EPB = 2, MINB = 2; static constexpr int FPI = 2; static constexpr bool LEAN = false; };
+template <> struct Tile<6, 4> : TilePick<ESDG_TUNE_T64E, ESDG_TUNE_T64M> { static constexpr int FPI = 1; static constexpr bool LEAN = false; };
+template <> struct Tile<7, 4> : TilePick<ESDG_TUNE_T74E, ESDG_TUNE_T74M> { static constexpr int FPI = 1; static constexpr bool LEAN = false; };
+template <> struct Tile<8, 4> : TilePick<ESDG_TUNE_T84E, ESDG_TUNE_T84M> { static constexpr int FPI = 2; static constexpr bool LEAN = false; };
 
 // Shared-memory layout of the nine node quantities: three arrays of PAIRS --
 // (rho/2, b), (log rho/2, log b), (phi/2, 1/(2b)) -- followed by the three
