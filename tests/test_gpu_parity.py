@@ -208,6 +208,27 @@ def test_partition_bitwise_trajectory(port, ranks, path):
     assert np.array_equal(states[0], states[1])
 
 
+@pytest.mark.parametrize("path", [capi.PATH_SPLIT, capi.PATH_STAGE])
+def test_one_element_per_partition(port, path):
+    """The finest partition make_partition allows (partition.cpp:13-30): one
+    element per rank, every face a ghost face -- bitwise the one-partition
+    result; one rank more is rejected like the reference's
+    std::invalid_argument("more ranks than elements")."""
+    res = []
+    for ranks in (1, 8):
+        o, g = make(port, "bubble", (1, False), 3, ranks=ranks, path=path)
+        q = o.init_case(po.CASE_ENTROPY_TEST, 3).copy()
+        rhs = g.assemble_rhs(q)
+        g.set_state(q)
+        for _ in range(3):
+            g.step(1e-3)
+        res.append((rhs, g.get_state(), g.quadrature_total(0), g.compute_dt(0.5)))
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    assert res[0][3] == res[1][3] and abs(res[0][2] - res[1][2]) <= 1e-14 * abs(res[0][2])
+    with pytest.raises(capi.EsdgError, match="more ranks than elements"):
+        make(port, "bubble", (1, False), 3, ranks=9, path=path)
+
+
 @pytest.mark.parametrize("path", [capi.PATH_FUSED, capi.PATH_STAGE])
 @pytest.mark.parametrize("ranks,order", [(2, 3), (3, 4), (5, 2)])
 def test_one_pass_overlap_bitwise(port, ranks, order, path):
