@@ -426,6 +426,19 @@ def test_baroclinic_jet_discrete_balance(port):
     assert float(np.abs(q2[:, 2:4] / q2[:, :1]).max()) <= 5e-2   # measured 1.2e-2, thin air at the lid
 
 
+def test_dt_calibration_acceptance_8():
+    """acceptance.cpp:302-335 (criterion 8): the N = 4, L = 6 rising-bubble
+    configuration at Courant 0.5 gives dt = 8.18e-3 s +- 15 % -- here from the
+    device-side minimum reduction (K6) over 3.3e7 nodes, which also equals the
+    host evaluation bitwise."""
+    g = capi.GpuSolver(capi.Mesh(capi.bubble_mesh_config(6, False)), 4, "f64")
+    g.init_case(capi.CASE_BUBBLE_SHARP)
+    dt = g.compute_dt(0.5)
+    assert abs(dt - 8.18e-3) / 8.18e-3 <= 0.15, dt
+    g.set_reduction(capi.REDUCE_ON_HOST)
+    assert g.compute_dt(0.5) == dt
+
+
 def test_init_case_matches_oracle(port):
     for case, seed in ((po.CASE_BUBBLE_SHARP, 0), (po.CASE_BUBBLE_SMOOTH, 0), (po.CASE_HYDROSTATIC, 0),
                        (po.CASE_ENTROPY_TEST, 77)):

@@ -208,3 +208,23 @@ def test_library_is_a_product_build():
     flags = open(os.path.join(capi.CSRC, "build", ".flags")).read()
     assert "ESDG_LADDER" not in flags and "ESDG_TUNE" not in flags, flags
     assert "arch=compute_100a,code=sm_100a" in flags and "-lineinfo" in flags
+
+
+def test_lsrk_temporal_order():
+    """acceptance.cpp:363-392 (criterion 10): lsrk_step with the exported
+    Carpenter-Kennedy coefficients integrates q' = -q to t = 1 with observed
+    order 4.0 +- 0.1 between dt = 0.1, 0.05, 0.025, 0.0125."""
+    a, b, c = capi.lsrk_coefficients()
+    assert a[0] == 0.0 and c[0] == 0.0
+
+    def run(dt):
+        q, k = 1.0, 0.0
+        for _ in range(int(round(1.0 / dt))):
+            for s in range(5):      # time_integration.hpp:43-49
+                k = a[s] * k + dt * (-q)
+                q += b[s] * k
+        return abs(q - np.exp(-1.0))
+
+    errs = [run(dt) for dt in (0.1, 0.05, 0.025, 0.0125)]
+    orders = [np.log2(errs[i] / errs[i + 1]) for i in range(3)]
+    assert min(orders) >= 3.9 and max(orders) <= 4.1, orders
