@@ -327,13 +327,14 @@ def main_b200(args, rank, local_rank, world):
             solver.step(dt, check_state=True)
             capi.check(L.esdg_b200_solver_get_state(solver.h, capi.REG_Q, host_q.data_ptr()))
 
-        # (b) step, then the result goes to the host while the next step's input
-        # comes in (esdg_b200_solver_swap_state: chunk-pipelined, full duplex;
-        # every step still moves its input H2D and its result D2H)
+        # (b) one call per step: the result goes to the host while the next
+        # step's input comes in (chunk-pipelined, full duplex), and the runs of
+        # the last stage that have finished leave while the rest still computes
+        # (esdg_b200_solver_step_swap; every step still moves its input H2D and
+        # its result D2H, and reports a non-physical state)
         def duplex():
-            solver.step(dt, check_state=True)
-            capi.check(L.esdg_b200_solver_swap_state(solver.h, capi.REG_Q, host_q.data_ptr(),
-                                                     host_q.data_ptr()))
+            capi.check(L.esdg_b200_solver_step_swap(solver.h, dt, host_q.data_ptr(), host_q.data_ptr(), 1),
+                       solver.h)
 
         seq_value = timed(sequential)
         capi.check(L.esdg_b200_solver_set_state(solver.h, capi.REG_Q, host_q.data_ptr()))
@@ -341,8 +342,9 @@ def main_b200(args, rank, local_rank, world):
         e2e = {"value": dup_value, "unit": UNIT,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                "steps": e2e_steps,
-               "call": "esdg_b200_solver_step + esdg_b200_solver_swap_state (result to the pinned host "
-                       "StateField while the next step's input is uploaded from it, chunk-pipelined)",
+               "call": "esdg_b200_solver_step_swap (one LSRK step; the result goes to the pinned host "
+                       "StateField, run by run of the last stage, while the next step's input is "
+                       "uploaded from it, chunk-pipelined)",
                "sequential_value": seq_value,
                "sequential_call": "esdg_b200_solver_set_state + esdg_b200_solver_step + "
                                   "esdg_b200_solver_get_state on pinned host StateField buffers"}

@@ -391,6 +391,13 @@ int esdg_b200_solver_get_state(esdg_b200_solver* s, int reg, void* host);
  * memory is needed for the two directions to overlap. */
 int esdg_b200_solver_swap_state(esdg_b200_solver* s, int reg, const void* host_in,
                                 void* host_out);
+/* esdg_b200_solver_step followed by esdg_b200_solver_swap_state(REG_Q, ...),
+ * with the last LSRK stage cut into runs of elements so that finished runs
+ * leave for host_out while the rest of the stage is still computing; the same
+ * result bitwise. check != 0: report a non-physical state like
+ * esdg_b200_solver_step does (after the transfers). */
+int esdg_b200_solver_step_swap(esdg_b200_solver* s, double dt,
+                               const void* host_in, void* host_out, int check);
 /* phi() (solver.hpp:79), local range */
 int esdg_b200_solver_get_phi(esdg_b200_solver* s, void* host);
 

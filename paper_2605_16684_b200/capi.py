@@ -138,6 +138,7 @@ SIGNATURES = {
     "esdg_b200_solver_set_state": (_i, [_vp, _i, _vp]),
     "esdg_b200_solver_get_state": (_i, [_vp, _i, _vp]),
     "esdg_b200_solver_swap_state": (_i, [_vp, _i, _vp, _vp]),
+    "esdg_b200_solver_step_swap": (_i, [_vp, _d, _vp, _vp, _i]),
     "esdg_b200_solver_get_phi": (_i, [_vp, _vp]),
     "esdg_b200_solver_assemble_rhs": (_i, [_vp, _vp, _vp, _d, _d]),
     "esdg_b200_solver_volume_rhs": (_i, [_vp, _vp, _vp]),
@@ -433,6 +434,18 @@ class GpuSolver:
         assert q_out.shape == self.shape and q_out.dtype == self.dtype and q_out.flags.c_contiguous
         self._chk(lib().esdg_b200_solver_swap_state(self.h, reg, q_in.ctypes.data_as(_vp),
                                                     q_out.ctypes.data_as(_vp)))
+        return q_out
+
+    def step_swap(self, dt, q_in, q_out=None, check_state=True):
+        """One LSRK step, then the result to q_out and q_in in as the next
+        state; finished parts of the last stage leave while it still runs."""
+        q_in = np.ascontiguousarray(q_in, self.dtype)
+        assert q_in.shape == self.shape
+        if q_out is None:
+            q_out = np.empty(self.shape, self.dtype)
+        assert q_out.shape == self.shape and q_out.dtype == self.dtype and q_out.flags.c_contiguous
+        self._chk(lib().esdg_b200_solver_step_swap(self.h, dt, q_in.ctypes.data_as(_vp),
+                                                   q_out.ctypes.data_as(_vp), 1 if check_state else 0))
         return q_out
 
     def get_phi(self):

@@ -26,7 +26,8 @@ cudaError_t launch_one(const dev::RhsParams<Real, NQ>& P, long long n_groups,
   });
   if (attr_err != cudaSuccess) return attr_err;
   if (P.ne <= 0) return cudaSuccess;
-  const long long blocks = P.groups ? n_groups : (P.ne + EPB - 1) / EPB;
+  // n_groups > 0 without a list: the run of groups starting at P.group_base
+  const long long blocks = (P.groups || n_groups > 0) ? n_groups : (P.ne + EPB - 1) / EPB;
   if (blocks <= 0) return cudaSuccess;
   kern<<<dim3(unsigned(blocks)), dim3(T), smem, stream>>>(P);
   return cudaGetLastError();

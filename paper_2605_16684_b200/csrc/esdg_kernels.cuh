@@ -69,6 +69,7 @@ struct RhsParams {
   // interior / boundary lists let the one-pass kernels overlap the halo
   // exchange the way the reference's volume phase does (solver.hpp:259-262).
   const int32_t* groups;
+  int group_base; // groups == null: CTA i works on group group_base + i
   unsigned long long* flag;
   FlagRecord* flag_records;
   long long ne;
@@ -597,7 +598,8 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
 
   const int tid = threadIdx.x;
   const long long e0 =
-      static_cast<long long>(P.groups ? P.groups[blockIdx.x] : int32_t(blockIdx.x)) * EPB;
+      static_cast<long long>(P.groups ? P.groups[blockIdx.x]
+                                      : int32_t(blockIdx.x) + P.group_base) * EPB;
 #ifdef ESDG_TUNE_PHASE_CLOCKS
   long long tclk[10];
   int nclk = 0;

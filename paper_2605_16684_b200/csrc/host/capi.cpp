@@ -313,6 +313,11 @@ int esdg_b200_solver_step(esdg_b200_solver* s, double dt, int check) {
   CORE(s);
   return c.step(dt, check != 0);
 }
+int esdg_b200_solver_step_swap(esdg_b200_solver* s, double dt, const void* host_in, void* host_out,
+                               int check) {
+  CORE(s);
+  return c.step_swap(dt, host_in, host_out, check != 0);
+}
 int esdg_b200_solver_sync(esdg_b200_solver* s) { CORE(s); return c.sync(); }
 int esdg_b200_solver_compute_dt(esdg_b200_solver* s, double courant, double* dt) {
   CORE(s);

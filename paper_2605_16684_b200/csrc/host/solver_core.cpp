@@ -162,6 +162,7 @@ SolverCore::~SolverCore() {
   for (auto& ls : shards_) {
     if (ls.dev) cudaSetDevice(ls.dev->device());
     if (ls.comm) cudaStreamDestroy(ls.comm);
+    if (ls.down) cudaStreamDestroy(ls.down);
     if (ls.ev_pack) cudaEventDestroy(ls.ev_pack);
     if (ls.ev_recv) cudaEventDestroy(ls.ev_recv);
     if (ls.ev_surf) cudaEventDestroy(ls.ev_surf);
@@ -641,6 +642,84 @@ int SolverCore::step(double dt, bool do_check) {
       RC(axpy(bs));
     }
   }
+  if (do_check) return check();
+  return ESDG_B200_OK;
+}
+
+// step() followed by swap_state(REG_Q, host_in, host_out), with the last
+// stage cut into runs of element groups so that the result of a run leaves
+// for the host while the following runs are still being computed (a coupled
+// driver that hands the state to host code every step, the reference's
+// Solver::state() contract, solver.hpp:74-89). The upload of the next input
+// follows each piece's download as in swap_state; it writes the q buffer the
+// last stage has just filled, which the stage's remaining runs never read
+// (they read the previous buffer and k). One partition without halo on the
+// stage path; everything else takes the plain sequence.
+int SolverCore::step_swap(double dt, const void* host_in, void* host_out, bool do_check) {
+  if (!host_in || !host_out) return ESDG_B200_BADARG;
+  if (shards_.size() != 1 || any_halo_ || path_ != ESDG_B200_PATH_STAGE) {
+    const int rc = step(dt, do_check);
+    if (rc != ESDG_B200_OK) return rc;
+    return swap_state(ESDG_B200_REG_Q, host_in, host_out);
+  }
+  LocalShard& ls = shards_[0];
+  CU(cudaSetDevice(ls.dev->device()));
+  if (!ls.down) CU(cudaStreamCreateWithFlags(&ls.down, cudaStreamNonBlocking));
+  double a[5], b[5], c[5];
+  lsrk_coefficients(a, b, c);
+  auto rounded = [&](double x) { return opt_.precision == 8 ? x : double(float(x)); };
+  const int source = opt_.settings.coriolis_mode != 0 ? 1 : 0;
+  for (int s = 0; s < 4; ++s) RC(stage_fused(rounded(a[s]), dt, rounded(b[s]), s));
+  const int64_t ne = ls.end - ls.begin;
+  const int epb = ls.dev->elements_per_group();
+  const int64_t groups = (ne + epb - 1) / epb;
+  constexpr int kRuns = 8;
+  const size_t per = size_t(opt_.precision) * 5 * size_t(n3_);
+  const int64_t piece = std::max<int64_t>(1, (int64_t(32) << 20) / int64_t(per));
+  cudaStream_t compute = ls.dev->stream(), down = ls.down, up = ls.comm;
+  cudaEvent_t ev_run[kRuns] = {}, ev_piece = nullptr;
+  int rc = ESDG_B200_OK;
+  auto cleanup = [&] {
+    for (auto& e : ev_run)
+      if (e) cudaEventDestroy(e);
+    if (ev_piece) cudaEventDestroy(ev_piece);
+  };
+  for (auto& e : ev_run)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) rc = ESDG_B200_CUDA;
+  if (cudaEventCreateWithFlags(&ev_piece, cudaEventDisableTiming) != cudaSuccess) rc = ESDG_B200_CUDA;
+  int64_t run_end[kRuns];
+  for (int r = 0; r < kRuns && rc == ESDG_B200_OK; ++r) {
+    const int64_t g0 = groups * r / kRuns, g1 = groups * (r + 1) / kRuns;
+    run_end[r] = std::min<int64_t>(ne, g1 * epb);
+    rc = timed(ls, kClsVolume, [&] {
+      return ls.dev->stage_fused_range(rounded(a[4]), dt, rounded(b[4]), source, 4, g0, g1 - g0,
+                                       r == kRuns - 1, nullptr);
+    });
+    if (rc == ESDG_B200_OK && cudaEventRecord(ev_run[r], compute) != cudaSuccess) rc = ESDG_B200_CUDA;
+  }
+  // all runs are enqueued and REG_Q names the new buffer: move it, run by run
+  int64_t first = 0;
+  for (int r = 0; r < kRuns && rc == ESDG_B200_OK; ++r) {
+    if (cudaStreamWaitEvent(down, ev_run[r], 0) != cudaSuccess) rc = ESDG_B200_CUDA;
+    for (int64_t count = 0; first < run_end[r] && rc == ESDG_B200_OK; first += count) {
+      count = std::min(piece, run_end[r] - first);
+      const size_t off = size_t(first) * per;
+      rc = ls.dev->download(ESDG_B200_REG_Q, static_cast<char*>(host_out) + off, first, count, down, true);
+      if (rc != ESDG_B200_OK) break;
+      if (cudaEventRecord(ev_piece, down) != cudaSuccess || cudaStreamWaitEvent(up, ev_piece, 0) != cudaSuccess) {
+        rc = ESDG_B200_CUDA;
+        break;
+      }
+      rc = ls.dev->upload(ESDG_B200_REG_Q, static_cast<const char*>(host_in) + off, first, count, up, true);
+    }
+  }
+  const cudaError_t e0 = cudaStreamSynchronize(compute), e1 = cudaStreamSynchronize(down),
+                    e2 = cudaStreamSynchronize(up);
+  cleanup();
+  if (rc != ESDG_B200_OK) return rc;
+  if (e0 != cudaSuccess) return cuda_fail(e0, "step_swap");
+  if (e1 != cudaSuccess) return cuda_fail(e1, "step_swap");
+  if (e2 != cudaSuccess) return cuda_fail(e2, "step_swap");
   if (do_check) return check();
   return ESDG_B200_OK;
 }

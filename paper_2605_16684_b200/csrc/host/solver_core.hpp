@@ -47,6 +47,7 @@ public:
   const Mesh& mesh() const { return *mesh_; }
 
   int set_path(int path);
+  int step_swap(double dt, const void* host_in, void* host_out, bool do_check);
   void set_overlap(bool on) { overlap_ = on; }
   void overlap_elements(int64_t* interior, int64_t* total);
   int set_settings(const esdg_b200_settings& s);
@@ -87,7 +88,7 @@ private:
     int64_t begin = 0, end = 0;
     RankHalo halo;
     std::unique_ptr<ShardBase> dev;
-    cudaStream_t comm = nullptr;
+    cudaStream_t comm = nullptr, down = nullptr; // copy streams (down: step_swap's D2H)
     cudaEvent_t ev_pack = nullptr, ev_recv = nullptr, ev_surf = nullptr;
   };
   struct TimedLaunch {

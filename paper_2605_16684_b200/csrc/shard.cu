@@ -321,6 +321,29 @@ public:
     return rc;
   }
 
+  int stage_fused_range(double a_old, double a_new, double b, int with_source, int stage,
+                        int64_t first_group, int64_t n_groups, bool last,
+                        cudaStream_t st) override {
+    const int64_t total = (ne_ + epb_ - 1) / epb_;
+    if (first_group < 0 || n_groups < 0 || first_group + n_groups > total)
+      return bad("stage_fused_range: bad group range");
+    CU(cudaSetDevice(device_));
+    if (!q_alt_) {
+      const size_t state_bytes = sizeof(Real) * size_t(ne_) * 5 * size_t(n3_);
+      CU(cudaMalloc(&q_alt_, state_bytes + 64));
+    }
+    int rc = ESDG_B200_OK;
+    if (n_groups > 0) {
+      range_first_ = first_group;
+      range_count_ = n_groups;
+      rc = launch(kModeFused, 0, 1, a_old, a_new, b, q_alt_, with_source, stage, ESDG_B200_PART_ALL, st);
+      range_first_ = range_count_ = 0;
+    }
+    if (rc == ESDG_B200_OK && last) std::swap(q_, q_alt_);
+    return rc;
+  }
+  int elements_per_group() const override { return epb_; }
+
   int64_t part_elements(int part) const override {
     return part == ESDG_B200_PART_ALL        ? ne_
            : part == ESDG_B200_PART_INTERIOR ? n_part_elems_[0]
@@ -332,7 +355,7 @@ public:
              Real* q_next, int with_source, int stage, int part, cudaStream_t st) {
     CU(cudaSetDevice(device_));
     const int32_t* groups = part == ESDG_B200_PART_ALL ? nullptr : groups_ + (part == ESDG_B200_PART_BOUNDARY ? n_groups_[0] : 0);
-    const long long n_groups = part == ESDG_B200_PART_ALL ? 0 : n_groups_[part - 1];
+    const long long n_groups = part == ESDG_B200_PART_ALL ? range_count_ : n_groups_[part - 1];
     if (part != ESDG_B200_PART_ALL && n_groups == 0) return ESDG_B200_OK;
     cudaError_t e = cudaErrorInvalidValue;
     switch (nq_) {
@@ -470,6 +493,7 @@ private:
                       const int32_t* groups, long long n_groups, cudaStream_t st) {
     dev::RhsParams<Real, NQ> P;
     P.groups = groups;
+    P.group_base = groups ? 0 : int(range_first_);
     P.q = reg_ptr(src);
     P.q_next = q_next;
     P.b_upd = Real(b);
@@ -528,6 +552,7 @@ private:
 #undef ESDG_CASE
       default: return bad("unsupported nq");
     }
+    epb_ = epb;
     const int64_t ng = (ne_ + epb - 1) / epb;
     std::vector<int32_t> interior, boundary;
     n_part_elems_[0] = n_part_elems_[1] = 0;
@@ -605,6 +630,8 @@ private:
   int32_t *nbr_ = nullptr, *send_elem_ = nullptr, *send_face_ = nullptr,
           *ylevel_ = nullptr, *groups_ = nullptr;
   int64_t n_groups_[2] = {0, 0}, n_part_elems_[2] = {0, 0};
+  int64_t range_first_ = 0, range_count_ = 0; // stage_fused_range: groups of this launch
+  int epb_ = 1;
   unsigned long long *flag_ = nullptr, *flag_host_ = nullptr;
   double *red_out_ = nullptr, *red_tab_ = nullptr;
   unsigned* red_bad_ = nullptr;

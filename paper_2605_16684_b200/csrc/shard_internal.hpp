@@ -39,6 +39,14 @@ public:
   virtual int stage_fused(double a_old, double a_new, double b, int with_source,
                           int stage, int part, cudaStream_t st) = 0;
   virtual int64_t part_elements(int part) const = 0;
+  // the same stage on the run of element groups [first_group, first_group +
+  // n_groups) only (a group = elements_per_group() consecutive elements);
+  // the q buffers swap when `last` is set. Lets a driver start moving
+  // finished elements while the rest of the stage is still running.
+  virtual int stage_fused_range(double a_old, double a_new, double b, int with_source,
+                                int stage, int64_t first_group, int64_t n_groups, bool last,
+                                cudaStream_t st) = 0;
+  virtual int elements_per_group() const = 0;
   virtual int axpy(double b, cudaStream_t st) = 0;
   virtual int check(cudaStream_t st, int src, esdg_b200_error* err) = 0;
   // K6: one partial per element, see esdg_b200_shard_reduce

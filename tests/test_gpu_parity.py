@@ -566,3 +566,34 @@ def test_swap_state_equals_get_then_set(port):
         buf = q0.copy()                      # aliased: download, then upload the same chunk
         g.swap_state(buf, buf)
         assert np.array_equal(buf, q1) and np.array_equal(g.get_state(), q1)
+
+
+@pytest.mark.parametrize("ranks", [1, 2])
+@pytest.mark.parametrize("order,prec", [(4, "f64"), (3, "f32"), (5, "f64")])
+def test_step_swap_equals_step_then_swap(port, order, prec, ranks):
+    """esdg_b200_solver_step_swap: the last stage runs in eight runs of element
+    groups whose results leave for the host while the rest still computes
+    (one partition), or falls back to step + swap_state (several): either way
+    the downloaded result, the state left on the device and the k register
+    are bitwise those of the plain sequence, step after step."""
+    oc, _ = both_configs("bubble", 2, False)
+    o = port.mesh(oc).solver(order, prec)
+    q0 = o.init_case(po.CASE_BUBBLE_SMOOTH).copy()
+    nxt = o.init_case(po.CASE_ENTROPY_TEST, 9).copy()
+    res = []
+    for fused_call in (False, True):
+        _, g = make(port, "bubble", (2, False), order, prec=prec, ranks=ranks, path=capi.PATH_STAGE)
+        g.set_state(q0)
+        outs = []
+        for step in range(3):
+            q_in = nxt if step == 1 else None
+            if fused_call:
+                cur = g.step_swap(1e-3, q_in if q_in is not None else outs[-1] if outs else q0)
+            else:
+                g.step(1e-3)
+                cur = g.swap_state(q_in if q_in is not None else outs[-1] if outs else q0)
+            outs.append(cur.copy())
+        res.append((outs, g.get_state(), g.get_state(capi.REG_K)))
+    for a, b in zip(res[0][0], res[1][0]):
+        assert np.array_equal(a, b)
+    assert np.array_equal(res[0][1], res[1][1]) and np.array_equal(res[0][2], res[1][2])
