@@ -11,4 +11,10 @@ for prec in ("f64", "f32"):
         for path in (capi.PATH_SPLIT, capi.PATH_FUSED, capi.PATH_STAGE):
             s.set_path(path)
             s.step(1e-3)
+        q_host = s.get_state()
+        s.step_swap(1e-3, q_host, q_host)          # one partition only: falls back here (3 partitions)
+        s1 = capi.GpuSolver(mesh, order, prec)
+        s1.set_path(capi.PATH_STAGE)
+        s1.init_case(capi.CASE_BUBBLE_SMOOTH)
+        s1.step_swap(1e-3, s1.get_state())         # last stage in runs of element groups
         print(prec, order, float(np.abs(s.get_state()).max()), s.compute_dt(0.5), s.total_entropy())
