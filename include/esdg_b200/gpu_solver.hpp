@@ -185,6 +185,9 @@ public:
   void set_fused(bool on) {
     check(esdg_b200_solver_set_path(solver_, on ? ESDG_B200_PATH_FUSED : ESDG_B200_PATH_SPLIT));
   }
+  // ESDG_B200_PATH_SPLIT (the reference's structure, default), _FUSED, or _STAGE
+  // (one kernel per LSRK stage in step(): the fastest; same results as _FUSED)
+  void set_path(int path) { check(esdg_b200_solver_set_path(solver_, path)); }
   void set_dissipation(bool on) {
     settings_.dissipation = on;
     const esdg_b200_settings st{on ? 1 : 0, settings_.coriolis_mode, settings_.f0,
