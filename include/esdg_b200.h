@@ -312,7 +312,7 @@ enum {
 enum {
   ESDG_B200_PATH_SPLIT = 0, /* K1 then K2, as the reference structures it */
   ESDG_B200_PATH_FUSED = 1, /* K1+K2 in one kernel */
-  ESDG_B200_PATH_STAGE = 2  /* step(): K1+K2+K3 in one kernel per stage;
+  ESDG_B200_PATH_STAGE = 2  /* default. step(): K1+K2+K3 in one kernel per stage;
                                rhs()/assemble_rhs() behave like PATH_FUSED */
 };
 

@@ -185,8 +185,9 @@ public:
   void set_fused(bool on) {
     check(esdg_b200_solver_set_path(solver_, on ? ESDG_B200_PATH_FUSED : ESDG_B200_PATH_SPLIT));
   }
-  // ESDG_B200_PATH_SPLIT (the reference's structure, default), _FUSED, or _STAGE
-  // (one kernel per LSRK stage in step(): the fastest; same results as _FUSED)
+  // ESDG_B200_PATH_STAGE (default: one kernel per LSRK stage in step(), the
+  // fastest; assemble_rhs as _FUSED), _FUSED, or _SPLIT (the reference's
+  // volume -> surface -> axpy structure)
   void set_path(int path) { check(esdg_b200_solver_set_path(solver_, path)); }
   void set_dissipation(bool on) {
     settings_.dissipation = on;

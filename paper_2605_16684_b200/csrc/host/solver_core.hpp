@@ -121,7 +121,7 @@ private:
   std::vector<int64_t> range_begin_;
   int64_t local_begin_ = 0, local_end_ = 0;
   std::vector<LocalShard> shards_;
-  int path_ = ESDG_B200_PATH_SPLIT;
+  int path_ = ESDG_B200_PATH_STAGE; // the fastest; SPLIT keeps the reference's kernel structure
   int reduction_ = ESDG_B200_REDUCE_ON_DEVICE;
   bool any_halo_ = false;
   bool overlap_ = true; // one-pass paths: interior groups hide the exchange

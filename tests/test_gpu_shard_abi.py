@@ -133,6 +133,7 @@ def test_shard_abi_rhs_orders(setup):
     into interior and boundary element groups all reproduce the solver's RHS."""
     lib = capi.lib()
     mesh, ref, q, shards = setup
+    ref.set_path(capi.PATH_SPLIT)
     ref.set_state(q)
     ref.rhs(0.0, 1.0)
     want = ref.get_state(capi.REG_K)
