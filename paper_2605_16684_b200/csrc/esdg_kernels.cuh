@@ -80,6 +80,7 @@ struct RhsParams {
   Real negd[NQ * NQ];    // -(2 D_ij); with metric[d]: -(2 g_d D_ij), kernels.hpp:187, 224-225
   Real metric[3];        // g_d = 2 / dx_d
   Real lift[3];          // Operators::face_coef, kernels.hpp:86-88
+  int flat_phi;          // phi is constant along x and y lines (checked by the host)
   int prefetch_ctas;     // resident CTAs chip-wide: L2 prefetch distance
   int with_source;       // Coriolis on (commit_volume, solver.hpp:205-216)
   int dissipation;
@@ -245,6 +246,14 @@ template <> struct Tile<5, 8> { static constexpr int EPB = ESDG_TUNE_EPB, MINB =
 #define ESDG_TUNE_T84M 3
 #endif
 template <int E, int M> struct TilePick { static constexpr int EPB = E, MINB = M; };
+// FLATXY: a second, shorter instance of the line sweep without the gravity
+// term serves the x and y lines when the potential is constant along them
+// (RhsParams::flat_phi). It removes 6 of 52 FP64 instructions per pair there
+// but doubles the sweep's code: +5 % (FP64) / +3 % (FP32) at N=6, within
+// +-1 % at N <= 5 and -12 ... -16 % at N=7 (instruction cache), so only N=6
+// uses it, and only in the one-pass kernels (the volume-only kernel at N=6
+// loses 16 % with it).
+template <int NQ, int BYTES> struct FlatXY { static constexpr bool value = NQ == 7; };
 template <> struct Tile<6, 8> : TilePick<ESDG_TUNE_T68E, ESDG_TUNE_T68M> { static constexpr int FPI = 2; static constexpr bool LEAN = false; };
 template <> struct Tile<7, 8> : TilePick<ESDG_TUNE_T78E, ESDG_TUNE_T78M> { static constexpr int FPI = 2; static constexpr bool LEAN = true; };
 template <> struct Tile<8, 8> { static constexpr int EPB = 1, MINB = 3; static constexpr int FPI = 2; static constexpr bool LEAN = true; };
@@ -354,7 +363,7 @@ __device__ __forceinline__ Node<Real> rotate_node(const Real nv[V_COUNT],
 // FP64 pipe for three cycles instead of two). One code instance
 // serves the three directions (the instruction cache is a real constraint
 // for these fully unrolled bodies).
-template <class Real, int NQ, bool DIAG>
+template <class Real, int NQ, bool DIAG, bool FLAT>
 __device__ __forceinline__ void sweep_line(const RhsParams<Real, NQ>& P,
                                            const Real* vals, int VS, int base,
                                            int stride, int dir, Real (&acc)[NQ][5]) {
@@ -459,7 +468,14 @@ __device__ __forceinline__ void sweep_line(const RhsParams<Real, NQ>& P,
   }
   return;
 #endif
-  // off-diagonal pairs, each once (kernels.hpp:190-231)
+  // off-diagonal pairs, each once (kernels.hpp:190-231). FLAT: phi is the
+  // same at every node of this line (see pair_flux), the gravity term
+  // vanishes identically and <phi> is the line's phi.
+  Real phi_line = Real(0);
+  if (FLAT) {
+    if (kLean) load_cold(vals, VS, base, nd[0]);
+    phi_line = nd[0].hphi + nd[0].hphi;
+  }
 #pragma unroll
   for (int i = 0; i < NQ; ++i) {
 #pragma unroll
@@ -467,11 +483,11 @@ __device__ __forceinline__ void sweep_line(const RhsParams<Real, NQ>& P,
       if (j <= i) continue; // constant bounds keep the unroll total
       cold(i);
       cold(j);
-      const PairFlux<Real> pf = pair_flux(nd[i], nd[j], P.gas.cg);
+      const PairFlux<Real> pf = pair_flux<Real, FLAT>(nd[i], nd[j], P.gas.cg, phi_line);
       const Real cij = P.negd[i * NQ + j];
       const Real cji = P.negd[j * NQ + i];
-      const Real fni = fma_(pf.tg, nd[i].hib, pf.f[1]);
-      const Real fnj = fma_(-pf.tg, nd[j].hib, pf.f[1]);
+      const Real fni = FLAT ? pf.f[1] : fma_(pf.tg, nd[i].hib, pf.f[1]);
+      const Real fnj = FLAT ? pf.f[1] : fma_(-pf.tg, nd[j].hib, pf.f[1]);
       acc[i][0] = fma_(cij, pf.f[0], acc[i][0]);
       acc[i][1] = fma_(cij, fni, acc[i][1]);
       acc[i][2] = fma_(cij, pf.f[2], acc[i][2]);
@@ -902,7 +918,12 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         for (int i = 0; i < NQ; ++i)
 #pragma unroll
           for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
-        sweep_line<Real, NQ, !(VOL && SURF)>(P, vals, VS, base, stride, dir, acc);
+        // x and y lines of a Cartesian mesh see a constant potential: no
+        // gravity term there (a second, shorter code instance of the sweep)
+        if (FlatXY<NQ, sizeof(Real)>::value && SURF && P.flat_phi && dir < 2)
+          sweep_line<Real, NQ, !(VOL && SURF), true>(P, vals, VS, base, stride, dir, acc);
+        else
+          sweep_line<Real, NQ, !(VOL && SURF), false>(P, vals, VS, base, stride, dir, acc);
         if (dir < 2) {
           // un-rotate into the slab: normal -> 1+dir, then cyclic. Without
           // faces the x sweep is the slab's first writer and simply stores;

@@ -206,6 +206,23 @@ public:
     CU(cudaMemset(q_, 0, state_bytes));
     CU(cudaMemset(k_, 0, state_bytes));
     CU(alloc_copy(&phi_, d.phi, sizeof(Real) * size_t(ne_) * size_t(n3_)));
+    {
+      // Is the potential constant along every x and y line (phi = g z on the
+      // reference's Cartesian lattice, solver.hpp:166-176)? Then the volume
+      // sweeps in x and y skip the gravity term, which is exactly zero there.
+      const Real* ph = static_cast<const Real*>(d.phi);
+      bool flat = true;
+      for (int64_t e = 0; e < ne_ && flat; ++e)
+        for (int c = 0; c < nq_ && flat; ++c) {
+          const Real* row = ph + size_t(e) * size_t(n3_) + size_t(c) * size_t(n2_);
+          for (int n = 1; n < n2_; ++n)
+            if (!(row[n] == row[0])) {
+              flat = false;
+              break;
+            }
+        }
+      flat_phi_ = flat ? 1 : 0;
+    }
     CU(alloc_copy(&nbr_, d.nbr, sizeof(int32_t) * size_t(ne_) * 6));
     {
       const int rc = build_groups(d.nbr);
@@ -532,6 +549,7 @@ private:
       P.prefetch_ctas = sm_count_ * per_sm;
     }
     P.dissipation = dissipation_;
+    P.flat_phi = flat_phi_;
     P.stage = stage;
     return launch_rhs<Real, NQ>(mode, P, n_groups, st);
   }
@@ -621,7 +639,7 @@ private:
   int nq_ = 0, n2_ = 0, n3_ = 0, device_ = -1, sm_count_ = 148;
   size_t smem_per_sm_ = 233472;
   int64_t ne_ = 0, elem_offset_ = 0, n_ghost_ = 0, n_send_ = 0;
-  int dissipation_ = 1, coriolis_mode_ = 0;
+  int dissipation_ = 1, coriolis_mode_ = 0, flat_phi_ = 0;
   Real metric_[3] = {0, 0, 0}, lift_[3] = {0, 0, 0};
   std::vector<Real> negd_;
   dev::GasParams<Real> gas_{};
