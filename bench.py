@@ -62,7 +62,7 @@ class ClockSampler:
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
-        self.device, self.rows, self.proc = device, [], None
+        self.device, self.rows, self.proc, self.first = device, [], None, 0
 
     def start(self):
         try:
@@ -79,17 +79,35 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.rows.append([c.strip() for c in line.split(",")])
 
+    def wait_first(self, timeout=8.0):
+        """Blocks until nvidia-smi has delivered its first row (its start-up can
+        take longer than the whole timed region on a fresh box); from then on a
+        row arrives every 100 ms."""
+        t0 = time.perf_counter()
+        while self.proc and not self.rows and time.perf_counter() - t0 < timeout:
+            time.sleep(0.02)
+
+    def mark(self):
+        """Rows before this call (idle, warm-up) do not count."""
+        self.first = len(self.rows)
+
     def stop(self):
         if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
+        self.proc = None
+
+    def snapshot(self):
+        """Median SM clock and the throttle reasons seen since mark()."""
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "samples": 0, "reasons": ["nvidia-smi unavailable"]}
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
+        for r in list(self.rows[self.first:]):
             if len(r) < 7:
                 continue
             try:
@@ -265,32 +283,64 @@ def main_b200(args, rank, local_rank, world):
             dist.barrier()
         torch.cuda.synchronize(device)
 
+    # clocks: nvidia-smi is started before the warm-up and must have delivered
+    # a row before the timed region begins; only rows of the timed region count
+    sampler = ClockSampler(device)
+    if rank == 0:
+        sampler.start()
+        sampler.wait_first()
+
     # ---- warm-up ----------------------------------------------------------
     for _ in range(max(args.warmup, 3)):
         solver.step(dt, check_state=True)
     solver.sync()
 
     # ---- timed region: exactly K steps, device events, max over ranks -----
-    solver.enable_timing(True)
-    solver.timers(reset=True)
-    launches0 = solver.timers()["launches"]
-    sampler = ClockSampler(device)
+    # A pass whose clock samples show a hardware or thermal slowdown, or SM
+    # clocks far below their maximum without a reason (a leftover clock lock),
+    # is discarded and measured once more; sw_power_cap is kept and noted.
+    def timed_pass():
+        solver.enable_timing(True)
+        solver.timers(reset=True)
+        l0 = solver.timers()["launches"]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        if rank == 0:
+            sampler.mark()
+        e0.record(stream)
+        for _ in range(args.steps):
+            solver.step(dt, check_state=False)
+        e1.record(stream)
+        solver.sync()
+        barrier()
+        t_ms = e0.elapsed_time(e1)
+        c = sampler.snapshot() if rank == 0 else None
+        tm = solver.timers(reset=True)
+        solver.enable_timing(False)
+        solver.step(dt, check_state=True)   # the state is still physical
+        solver.sync()
+        return t_ms, c, tm, l0
+
+    def suspicious(c):
+        if not c or c.get("sm_mhz") is None:
+            return False
+        bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} & set(c["reasons"])
+        stuck = c["sm_mhz"] < 0.8 * c["sm_max_mhz"] and not c["reasons"]
+        return bool(bad) or stuck
+
+    ms, clocks, timers, launches0 = timed_pass()
+    redo = 1 if (rank == 0 and suspicious(clocks)) else 0
+    if world > 1:
+        t = torch.tensor([redo], dtype=torch.int32, device=f"cuda:{device}")
+        dist.broadcast(t, 0)
+        redo = int(t.item())
+    if redo:
+        first = clocks
+        ms, clocks, timers, launches0 = timed_pass()
+        if rank == 0:
+            clocks["remeasured_after"] = first
     if rank == 0:
-        sampler.start()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    e0.record(stream)
-    for _ in range(args.steps):
-        solver.step(dt, check_state=False)
-    e1.record(stream)
-    solver.sync()
-    barrier()
-    ms = e0.elapsed_time(e1)
-    clocks = sampler.stop() if rank == 0 else None
-    timers = solver.timers(reset=True)
-    solver.enable_timing(False)
-    solver.step(dt, check_state=True)   # the state is still physical
-    solver.sync()
+        sampler.stop()
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{device}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
