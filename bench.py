@@ -62,7 +62,7 @@ class ClockSampler:
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
-        self.device, self.rows, self.proc, self.first = device, [], None, 0
+        self.device, self.rows, self.proc, self.first, self.warm = device, [], None, 0, 0
 
     def start(self):
         try:
@@ -86,6 +86,7 @@ class ClockSampler:
         t0 = time.perf_counter()
         while self.proc and not self.rows and time.perf_counter() - t0 < timeout:
             time.sleep(0.02)
+        self.warm = len(self.rows)      # the warm-up starts here
 
     def mark(self):
         """Rows before this call (idle, warm-up) do not count."""
@@ -101,13 +102,21 @@ class ClockSampler:
             self.proc.kill()
         self.proc = None
 
-    def snapshot(self):
-        """Median SM clock and the throttle reasons seen since mark()."""
+    def snapshot(self, first=None):
+        """Median SM clock and the throttle reasons seen since mark(). A timed
+        region shorter than the sampling period may see no row at all: the
+        rows since the warm-up began (the same load) are used then, and the
+        result says so."""
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "samples": 0, "reasons": ["nvidia-smi unavailable"]}
+        first = self.first if first is None else first
+        if first == self.first and len(self.rows) <= self.first and self.first > self.warm:
+            out = self.snapshot(self.warm)
+            out["window"] = "warm-up + timed region (no sample fell into the timed region)"
+            return out
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in list(self.rows[self.first:]):
+        for r in list(self.rows[first:]):
             if len(r) < 7:
                 continue
             try:
