@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <mutex>
@@ -673,21 +674,26 @@ int SolverCore::step_swap(double dt, const void* host_in, void* host_out, bool d
   const int64_t ne = ls.end - ls.begin;
   const int epb = ls.dev->elements_per_group();
   const int64_t groups = (ne + epb - 1) / epb;
-  constexpr int kRuns = 8;
+  constexpr int kMaxRuns = 32;
+  // tuning hooks (development): number of runs of the last stage, copy piece in MiB
+  static const int env_runs = std::getenv("ESDG_B200_SWAP_RUNS") ? std::atoi(std::getenv("ESDG_B200_SWAP_RUNS")) : 0;
+  static const int env_piece = std::getenv("ESDG_B200_SWAP_PIECE_MB") ? std::atoi(std::getenv("ESDG_B200_SWAP_PIECE_MB")) : 0;
+  const int kRuns = std::max(1, std::min(kMaxRuns, env_runs > 0 ? env_runs : 8));
   const size_t per = size_t(opt_.precision) * 5 * size_t(n3_);
-  const int64_t piece = std::max<int64_t>(1, (int64_t(32) << 20) / int64_t(per));
+  const int64_t piece =
+      std::max<int64_t>(1, (int64_t(env_piece > 0 ? env_piece : 32) << 20) / int64_t(per));
   cudaStream_t compute = ls.dev->stream(), down = ls.down, up = ls.comm;
-  cudaEvent_t ev_run[kRuns] = {}, ev_piece = nullptr;
+  cudaEvent_t ev_run[kMaxRuns] = {}, ev_piece = nullptr;
   int rc = ESDG_B200_OK;
   auto cleanup = [&] {
     for (auto& e : ev_run)
       if (e) cudaEventDestroy(e);
     if (ev_piece) cudaEventDestroy(ev_piece);
   };
-  for (auto& e : ev_run)
-    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) rc = ESDG_B200_CUDA;
+  for (int r = 0; r < kRuns; ++r)
+    if (cudaEventCreateWithFlags(&ev_run[r], cudaEventDisableTiming) != cudaSuccess) rc = ESDG_B200_CUDA;
   if (cudaEventCreateWithFlags(&ev_piece, cudaEventDisableTiming) != cudaSuccess) rc = ESDG_B200_CUDA;
-  int64_t run_end[kRuns];
+  int64_t run_end[kMaxRuns];
   for (int r = 0; r < kRuns && rc == ESDG_B200_OK; ++r) {
     const int64_t g0 = groups * r / kRuns, g1 = groups * (r + 1) / kRuns;
     run_end[r] = std::min<int64_t>(ne, g1 * epb);
