@@ -173,6 +173,11 @@ typedef struct orc_solver_f32 orc_solver_f32;
   /* abs-sum flux scale S_v: max over nodes of the sum of    \
    * absolute values of every term the RHS adds into that node. scale[5]. */  \
   int orc_flux_scale_##SUF(orc_solver_##SUF* s, const REAL* q, double* scale);\
+  /* the same over [elem_begin, elem_end) with supplied neighbour traces */    \
+  int orc_flux_scale_rank_##SUF(orc_solver_##SUF* s, const REAL* q,           \
+                                int64_t elem_begin, int64_t elem_end,         \
+                                const int32_t* ghost_slot_of_face,            \
+                                const REAL* ghost_traces, double* scale);     \
   /* pointwise physics for known-answer tests (physics.hpp, log_mean.hpp) */  \
   REAL orc_log_mean_##SUF(REAL am, REAL ap, REAL lam, REAL lap);              \
   int orc_node_vals_##SUF(const REAL* q5, REAL phi, REAL gamma, REAL* out8);  \

@@ -198,6 +198,8 @@ class Oracle:
                 sig(f"extract_trace_{suf}", None, [vp, rp, C.c_int64, C.c_int, C.c_int, rp])
                 sig(f"axpy_{suf}", None, [vp, R])
                 sig(f"flux_scale_{suf}", C.c_int, [vp, rp, dp])
+                sig(f"flux_scale_rank_{suf}", C.c_int,
+                    [vp, rp, C.c_int64, C.c_int64, C.POINTER(C.c_int32), rp, dp])
             else:
                 sig(f"perf_{suf}", None, [vp, dp, C.POINTER(C.c_uint64), C.c_int])
         if self.kind == "port":
@@ -448,6 +450,16 @@ class Solver:
     def flux_scale(self, q):
         s = np.zeros(5)
         if self._f("flux_scale")(self.h, self._ptr(q), s.ctypes.data_as(C.POINTER(C.c_double))):
+            self._raise()
+        return s
+
+    def flux_scale_rank(self, q, eb, ee, ghost_slot_of_face, ghost_traces):
+        gs = np.ascontiguousarray(ghost_slot_of_face, np.int32)
+        gt = np.ascontiguousarray(ghost_traces, self.dtype)
+        s = np.zeros(5)
+        if self._f("flux_scale_rank")(self.h, self._ptr(q), eb, ee,
+                                      gs.ctypes.data_as(C.POINTER(C.c_int32)), self._ptr(gt),
+                                      s.ctypes.data_as(C.POINTER(C.c_double))):
             self._raise()
         return s
 

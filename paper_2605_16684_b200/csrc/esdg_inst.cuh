@@ -1,5 +1,5 @@
 // esdg_inst.cuh -- body shared by inst_nq*.cu; define ESDG_NQ before including.
-#include <mutex>
+#include <atomic>
 
 #include "esdg_kernels.cuh"
 #include "esdg_launch.hpp"
@@ -7,6 +7,7 @@
 namespace esdg_b200 {
 
 namespace {
+constexpr int kMaxDevices = 64;
 template <class Real, int NQ, bool VOL, bool SURF>
 cudaError_t launch_one(const dev::RhsParams<Real, NQ>& P, long long n_groups,
                        cudaStream_t stream) {
@@ -18,13 +19,16 @@ cudaError_t launch_one(const dev::RhsParams<Real, NQ>& P, long long n_groups,
 #endif
   constexpr size_t smem = dev::SmemMap<Real, NQ, EPB>::kBytes + ESDG_TUNE_EXTRA_SMEM;
   auto kern = dev::rhs_kernel<Real, NQ, EPB, MINB, VOL, SURF>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(
-        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  });
-  if (attr_err != cudaSuccess) return attr_err;
+  // the opt-in is a property of the (kernel, device) pair: once per device
+  static std::atomic<bool> opted[kMaxDevices];
+  int device = 0;
+  cudaError_t err = cudaGetDevice(&device);
+  if (err != cudaSuccess) return err;
+  if (device < 0 || device >= kMaxDevices || !opted[device].load(std::memory_order_acquire)) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (err != cudaSuccess) return err;
+    if (device >= 0 && device < kMaxDevices) opted[device].store(true, std::memory_order_release);
+  }
   if (P.ne <= 0) return cudaSuccess;
   // n_groups > 0 without a list: the run of groups starting at P.group_base
   const long long blocks = (P.groups || n_groups > 0) ? n_groups : (P.ne + EPB - 1) / EPB;

@@ -2,6 +2,7 @@
 #include "solver_core.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -172,10 +173,11 @@ SolverCore::~SolverCore() {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
   }
-  for (auto& p : event_pool_) {
-    cudaEventDestroy(p.first);
-    cudaEventDestroy(p.second);
-  }
+  for (auto& pool : event_pool_)
+    for (auto& p : pool.second) {
+      cudaEventDestroy(p.first);
+      cudaEventDestroy(p.second);
+    }
 }
 
 int SolverCore::local_index_of_rank(int rank) const {
@@ -435,19 +437,23 @@ int SolverCore::init_case(int case_id, uint64_t iparam, const double* dparam) {
 template <class F>
 int SolverCore::timed(LocalShard& ls, int cls, F&& launch) {
   if (!timing_) return launch();
+  // events belong to the device they were created on: one pool per device
   std::pair<cudaEvent_t, cudaEvent_t> ev;
-  if (!event_pool_.empty()) {
-    ev = event_pool_.back();
-    event_pool_.pop_back();
+  const int device = ls.dev->device();
+  auto& pool = event_pool_[device];
+  CU(cudaSetDevice(device));
+  if (!pool.empty()) {
+    ev = pool.back();
+    pool.pop_back();
   } else {
-    CU(cudaSetDevice(ls.dev->device()));
     CU(cudaEventCreate(&ev.first));
     CU(cudaEventCreate(&ev.second));
   }
   CU(cudaEventRecord(ev.first, ls.dev->stream()));
   const int rc = launch();
+  CU(cudaSetDevice(device));
   CU(cudaEventRecord(ev.second, ls.dev->stream()));
-  pending_.push_back({ev.first, ev.second, cls});
+  pending_.push_back({ev.first, ev.second, cls, device});
   if (pending_.size() >= 4096) RC(collect_timers());
   return rc;
 }
@@ -458,7 +464,7 @@ int SolverCore::collect_timers() {
     float ms = 0.f;
     CU(cudaEventElapsedTime(&ms, t.a, t.b));
     seconds_[t.cls] += double(ms) * 1e-3;
-    event_pool_.push_back({t.a, t.b});
+    event_pool_[t.device].push_back({t.a, t.b});
   }
   pending_.clear();
   return ESDG_B200_OK;
@@ -554,6 +560,9 @@ int SolverCore::rhs(int src, int dst, double a_old, double a_new,
     // one-pass kernel: the element groups without a ghost face run while the
     // traces travel, the others after they have landed (solver.hpp:259-294)
     const bool split = halo && overlap_;
+    // wait-first order (set_overlap(0)): the one launch over all groups reads
+    // the ghost traces, so the compute streams wait for them BEFORE it
+    if (halo && !split) RC(exchange_end());
     for (auto& ls : shards_)
       RC(timed(ls, kClsVolume, [&] {
         return ls.dev->rhs(kModeFused, src, dst, a_old, a_new, source, stage,
@@ -561,7 +570,7 @@ int SolverCore::rhs(int src, int dst, double a_old, double a_new,
                                                            : ESDG_B200_PART_ALL,
                            nullptr);
       }));
-    if (halo) RC(exchange_end());
+    if (split) RC(exchange_end());
     for (auto& ls : shards_) {
       if (!halo || ls.halo.peers.empty()) continue;
       if (split)
@@ -600,6 +609,8 @@ int SolverCore::stage_fused(double a_old, double a_new, double b, int stage) {
   const bool split = halo && overlap_;
   const int source = opt_.settings.coriolis_mode != 0 ? 1 : 0;
   if (halo) RC(exchange_begin(ESDG_B200_REG_Q));
+  // wait-first order: see rhs()
+  if (halo && !split) RC(exchange_end());
   // groups without a ghost face first: they hide the transfer
   for (auto& ls : shards_)
     RC(timed(ls, kClsVolume, [&] {
@@ -608,7 +619,7 @@ int SolverCore::stage_fused(double a_old, double a_new, double b, int stage) {
                                                                  : ESDG_B200_PART_ALL,
                                  nullptr);
     }));
-  if (halo) RC(exchange_end());
+  if (split) RC(exchange_end());
   for (auto& ls : shards_) {
     if (!halo || ls.halo.peers.empty()) continue;
     if (split)
@@ -882,7 +893,7 @@ int SolverCore::total_entropy_host(double* out) {
   const double J = mesh_->jacobian, gamma = opt_.gas.gamma, grav = opt_.gas.gravity;
   const int prec = opt_.precision;
   Neumaier sum;
-  bool bad = false;
+  std::atomic<bool> bad{false};
   RC(for_each_element_chunk(ESDG_B200_REG_Q, -1, [&](int64_t first, int64_t count, const char* qd, const char*) {
     std::vector<double> eta(size_t(count) * size_t(n3_));
     parallel_for(count, [&](int64_t b, int64_t e) {
@@ -915,7 +926,7 @@ int SolverCore::entropy_production_host(double* out) {
   const double J = mesh_->jacobian, gamma = opt_.gas.gamma, grav = opt_.gas.gravity;
   const int prec = opt_.precision;
   Neumaier sum;
-  bool bad = false;
+  std::atomic<bool> bad{false};
   RC(for_each_element_chunk(ESDG_B200_REG_Q, ESDG_B200_REG_K, [&](int64_t first, int64_t count, const char* qd, const char* kd) {
     std::vector<double> term(size_t(count) * size_t(n3_));
     parallel_for(count, [&](int64_t b, int64_t e) {

@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -94,6 +95,7 @@ private:
   struct TimedLaunch {
     cudaEvent_t a, b;
     int cls;
+    int device;
   };
 
   SolverCore() = default;
@@ -128,7 +130,7 @@ private:
   esdg_b200_error err_{};
   bool timing_ = false;
   std::vector<TimedLaunch> pending_;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> event_pool_;
+  std::map<int, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> event_pool_; // per device
   double seconds_[4] = {0, 0, 0, 0};
 };
 

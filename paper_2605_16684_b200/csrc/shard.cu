@@ -259,10 +259,14 @@ public:
     CU(cudaSetDevice(device_));
     const size_t per = sizeof(Real) * 5 * size_t(n3_);
     Real* dst = reg_ptr(reg) + size_t(first) * 5 * size_t(n3_);
-    if (async)
+    if (async) {
       CU(cudaMemcpyAsync(dst, host, per * size_t(count), cudaMemcpyHostToDevice, pick(st)));
-    else
+    } else {
+      // kernels run on a non-blocking stream the legacy stream does not order
+      // against: whatever still reads or writes the register must finish first
+      CU(cudaStreamSynchronize(stream_));
       CU(cudaMemcpy(dst, host, per * size_t(count), cudaMemcpyHostToDevice));
+    }
     return ESDG_B200_OK;
   }
 

@@ -58,3 +58,62 @@ def state_error(got, want):
         d = float(np.abs(got[:, v].astype(np.float64) - want[:, v].astype(np.float64)).max())
         out.append(d / s if s > 0 else d)
     return out
+
+
+# ---- sampled comparison on meshes too large to assemble on one CPU core ----------
+
+def sample_ranges(ne, epb, runs, rng):
+    """Element ranges [b, e) to check: first and last CTA (the last one is
+    partial when epb does not divide ne), both sides of every step_swap run
+    boundary, and random places."""
+    groups = (ne + epb - 1) // epb
+    picks = [(0, 3), (ne - 3, ne), ((groups - 1) * epb - 2, min(ne, (groups - 1) * epb + 2))]
+    for r in range(1, runs):
+        g0 = groups * r // runs
+        picks.append((g0 * epb - 2, g0 * epb + 2))
+    for b in rng.integers(0, ne - 3, 40):
+        picks.append((int(b), int(b) + 3))
+    return [(max(0, b), min(ne, e)) for b, e in picks]
+
+
+def face_table(omesh):
+    """The oracle mesh's Face records (mesh.hpp:35-41) as a structured array."""
+    import ctypes as C
+    p = omesh.o.f("mesh_faces")(omesh.h)
+    dt = np.dtype([("minus_elem", "<i4"), ("plus_elem", "<i4"), ("dir", "u1"), ("minus_side", "u1"),
+                   ("reflecting", "u1"), ("pad", "u1")])
+    buf = (C.c_char * (omesh.nfaces * dt.itemsize)).from_address(C.addressof(p.contents))
+    return np.frombuffer(buf, dtype=dt)
+
+
+def check_samples(o, face_of, faces, q, got, ranges, tol):
+    """Oracle RHS of the element ranges (assemble_rhs_rank, the neighbours'
+    traces extracted from the full state like a rank's ghost traces) against
+    the same elements of the GPU result."""
+    slot = np.full(o.mesh.nfaces, -1, np.int32)
+    want = np.zeros(q.shape, q.dtype)          # lazily committed; only the samples are touched
+    worst, n = 0.0, 0
+    for b, e in ranges:
+        traces, used = [], []
+        for el in range(b, e):
+            for lf in range(6):
+                fid = int(face_of[el, lf])
+                f = faces[fid]
+                if f["reflecting"] or slot[fid] >= 0:
+                    continue
+                am_minus = int(f["minus_elem"]) == el and int(f["minus_side"]) == lf % 2
+                other = int(f["plus_elem"]) if am_minus else int(f["minus_elem"])
+                if b <= other < e:
+                    continue
+                oside = (1 - int(f["minus_side"])) if am_minus else int(f["minus_side"])
+                slot[fid] = len(traces)
+                used.append(fid)
+                traces.append(o.extract_trace(q, other, int(f["dir"]), oside))
+        gt = np.ascontiguousarray(np.stack(traces)) if traces else np.zeros((1, 5, o.nq * o.nq), q.dtype)
+        o.assemble_rhs_rank(q, want, 0.0, 1.0, b, e, slot, gt)
+        scale = o.flux_scale_rank(q, b, e, slot, gt)
+        worst = max(worst, scaled_error(got[b:e], want[b:e], scale))
+        n += e - b
+        slot[used] = -1
+    assert worst <= tol, f"{n} sampled elements: scaled error {worst:.3e}"
+    return worst, n

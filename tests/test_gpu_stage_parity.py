@@ -1,0 +1,140 @@
+"""Oracle parity of the path bench.py times by default (-m gpu): the
+one-kernel-per-stage path (PATH_STAGE, rhs_kernel<...,VOL,SURF> with the fused
+LSRK update) at every order and precision, with walls and periodic boundaries,
+on one and three partitions -- and at the size bench.py runs (BASELINE.json
+configs[1], 884,736 elements), where the oracle is evaluated on sampled
+elements only.
+
+The orders take different code: TMA slab commit for odd NQ, per-thread commit
+for even NQ (N = 1, 3, 5, 7), the lean line state at N = 6, 7, the flat x/y
+sweep at N = 6, paired faces per iteration at N = 3 and N >= 5.
+
+Tolerances as in test_gpu_parity.py: FP64 RHS 2e-12 of the abs-sum flux scale
+(typical 1e-13 .. 7e-13; 1.41e-12 once in 680 random trials, pinned below),
+FP32 3e-5; five-step states 1e-11 / 1e-4 of max|q_v| (measured 2e-12 / 2e-5).
+"""
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+from paper_2605_16684_b200 import capi
+from helpers import both_configs, check_samples, face_table, sample_ranges, scaled_error, state_error
+from test_gpu_parity import TOL32, TOL64, make
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("ranks", [1, 3])
+@pytest.mark.parametrize("periodic", [False, True], ids=["walls", "periodic"])
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("order", [1, 2, 3, 4, 5, 6, 7])
+def test_stage_path_rhs_and_trajectory(port, order, prec, periodic, ranks):
+    """RHS through rhs() (the stage kernel without the update) and five LSRK
+    steps through the stage kernel against the oracle's assemble_rhs / step.
+    64 elements: several CTAs at every order, partitions of 21-22 elements
+    whose element groups straddle partition boundaries."""
+    level = 2 if order <= 5 else 1
+    o, g = make(port, "bubble", (level, periodic), order, prec=prec, ranks=ranks, path=capi.PATH_STAGE)
+    q = o.init_case(po.CASE_ENTROPY_TEST, 1000 + 10 * order + ranks).copy()
+    scale = o.flux_scale(q)
+    tol_rhs, tol_q = (TOL64, 1e-11) if prec == "f64" else (TOL32, 1e-4)
+    want, got = o.assemble_rhs(q), g.assemble_rhs(q)
+    assert scaled_error(got, want, scale) <= tol_rhs
+    # accumulate form with the stage coefficients' signs (a_old < 0)
+    out0 = (np.random.default_rng(order).standard_normal(q.shape) * scale[None, :, None]).astype(q.dtype)
+    want = o.assemble_rhs(q, out0.copy(), -0.4178904745, 0.5)
+    got = g.assemble_rhs(q, out0.copy(), -0.4178904745, 0.5)
+    assert scaled_error(got, want, scale) <= tol_rhs
+    o.state[:] = q
+    g.set_state(q)
+    dt = o.compute_dt(0.4)
+    dt = float(np.float32(dt)) if prec == "f32" else dt
+    for _ in range(5):
+        o.step(dt)
+        g.step(dt)
+    gs = g.get_state()
+    err = state_error(gs, o.state)
+    assert err[0] <= tol_q and err[4] <= tol_q, err
+    mom = float(np.abs(o.state[:, 1:4]).max())
+    assert float(np.abs(gs[:, 1:4].astype(np.float64) - o.state[:, 1:4]).max()) <= 10 * tol_q * mom
+    # the k register the stage kernel leaves behind is the oracle's too
+    k_scale = dt * scale + 1e-300
+    assert scaled_error(g.get_state(capi.REG_K), o.kreg, k_scale) <= 50 * tol_rhs
+
+
+@pytest.mark.parametrize("path", [capi.PATH_SPLIT, capi.PATH_FUSED, capi.PATH_STAGE])
+@pytest.mark.parametrize("ranks", [1, 4])
+def test_fuzz_outlier_regression(port, path, ranks):
+    """The one trial of 680 randomised comparisons (tools/fuzz_parity.py seed 0,
+    trial 138; profiles/r1_fuzz_parity.txt) above the survey's 1e-12: N = 6,
+    walls, no dissipation, EntropyTestState seed 603644430. The energy
+    tendency differs by 1.41e-12 of its flux scale, every other variable by
+    <= 5e-16, for every a_new, path and partition count: a logarithmic mean next
+    to its series threshold xi^2 = 1e-8, where the device logarithm (0.53 ulp)
+    and glibc's (< 1 ulp) may differ by an ulp that the quotient amplifies by
+    1/(2 xi) = 5e3. This is why the stated FP64 bound is 2e-12 and not 1e-12;
+    the test pins the level so a regression of the logarithm or of the branch
+    selector shows up."""
+    o, g = make(port, "bubble", (1, False), 6, diss=False, ranks=ranks, path=path)
+    q = o.init_case(po.CASE_ENTROPY_TEST, 603644430).copy()
+    scale = o.flux_scale(q)
+    want, got = o.assemble_rhs(q), g.assemble_rhs(q)
+    per = [float(np.abs(got[:, v] - want[:, v]).max()) / scale[v] for v in range(5)]
+    assert max(per[:4]) <= 1e-14, per
+    assert per[4] <= 1.6e-12, per
+
+
+def test_rhs_against_unmodified_reference(ref, port):
+    """The GPU RHS compared DIRECTLY with the unmodified reference
+    (oracle/_ref/libesdg_ref.so, which travels to the GPU box prebuilt), not
+    only transitively through the restatement."""
+    for order, prec, tol in ((4, "f64", TOL64), (5, "f64", TOL64), (4, "f32", TOL32)):
+        oc, cc = both_configs("bubble", 1, True)
+        r = ref.mesh(oc).solver(order, prec)
+        p = port.mesh(oc).solver(order, prec)
+        g = capi.GpuSolver(capi.Mesh(cc), order, prec)
+        g.set_path(capi.PATH_STAGE)
+        q = r.init_case(po.CASE_ENTROPY_TEST, 20240501).copy()
+        want, got = r.assemble_rhs(q), g.assemble_rhs(q)
+        assert scaled_error(got, want, p.flux_scale(q)) <= tol
+
+
+# ---- bench size ---------------------------------------------------------------
+
+def test_bench_size_sampled_parity(port):
+    """BASELINE.json configs[1] as bench.py runs it: N = 4, base 3^3 at
+    refinement 5 = 884,736 elements (176,948 CTAs, ~400 resident waves, L2
+    prefetch distance logic, a last CTA with one element). One assemble_rhs on
+    the GPU; the oracle evaluates ~190 sampled elements (assemble_rhs_rank with
+    the neighbours' traces taken from the full state): first / last CTA, both
+    sides of the step_swap run boundaries and random places. Then one
+    step_swap (the call bench.py's e2e arm times) against step + get_state,
+    bitwise."""
+    cfg_o = po.bubble_mesh_config(5, False, base=(3, 3, 3))
+    cfg_g = capi.bubble_mesh_config(5, False, base=(3, 3, 3))
+    g = capi.GpuSolver(capi.Mesh(cfg_g), 4, "f64")
+    g.set_path(capi.PATH_STAGE)
+    g.init_case(capi.CASE_BUBBLE_SHARP)
+    q = g.get_state()
+    assert q.shape == (884736, 5, 125)
+    # a rough state on top of the bubble so that every term is exercised:
+    # smooth, deterministic, 1e-3 relative
+    rng = np.random.default_rng(5)
+    q *= 1.0 + 1e-3 * np.sin(np.arange(q.shape[0], dtype=np.float64) * 0.37)[:, None, None]
+    q[:, 1:4] += 0.5 * rng.standard_normal((q.shape[0], 3, 1))
+    got = g.assemble_rhs(q)
+    omesh = port.mesh(cfg_o)
+    o = omesh.solver(4, "f64")
+    faces, face_of = face_table(omesh), omesh.face_of
+    ranges = sample_ranges(q.shape[0], 5, 8, rng)
+    worst, n = check_samples(o, face_of, faces, q, got, ranges, TOL64)
+    print(f"bench-size parity: {n} sampled elements, scaled error {worst:.2e}")
+    # step_swap at this size: eight runs of the last stage leaving for the host
+    g.set_state(q)
+    dt = 0.5 * g.compute_dt(0.5)
+    out = g.step_swap(dt, q)
+    g2 = capi.GpuSolver(capi.Mesh(cfg_g), 4, "f64")
+    g2.set_path(capi.PATH_STAGE)
+    g2.set_state(q)
+    g2.step(dt)
+    assert np.array_equal(out, g2.get_state())

@@ -318,3 +318,23 @@ def test_lsrk_order_four(port):
             errs.append(float(np.abs(s.state - ref_state).max()))
     rate = math.log2(errs[2] / errs[1])
     assert 3.5 <= rate <= 5.2, (errs, rate)
+
+
+def test_sampled_assembly_equals_full_assembly(port):
+    """The machinery of tests/test_gpu_stage_parity.py's bench-size check:
+    assemble_rhs_rank on element ranges with the neighbours' traces taken from
+    the full state reproduces the full assembly bitwise on those elements, and
+    flux_scale_rank over ranges that cover the mesh gives flux_scale."""
+    from helpers import check_samples, face_table, sample_ranges
+    for periodic in (False, True):
+        omesh = port.mesh(po.bubble_mesh_config(2, periodic))
+        o = omesh.solver(3, "f64")
+        q = o.init_case(po.CASE_ENTROPY_TEST, 8).copy()
+        full = o.assemble_rhs(q)
+        rng = np.random.default_rng(1)
+        ranges = sample_ranges(omesh.ne, 5, 4, rng)
+        worst, n = check_samples(o, omesh.face_of, face_table(omesh), q, full, ranges, 0.0)
+        assert worst == 0.0 and n >= 100
+        slot = np.full(omesh.nfaces, -1, np.int32)
+        whole = o.flux_scale_rank(q, 0, omesh.ne, slot, np.zeros((1, 5, 16)))
+        assert np.array_equal(whole, o.flux_scale(q))

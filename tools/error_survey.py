@@ -27,7 +27,7 @@ for prec in ("f64", "f32"):
                 want = o.assemble_rhs(q)
                 wv = o.volume_rhs(q)
                 out = [f"{prec} {kind}{margs} case{case} N={order} diss={int(diss)}"]
-                for path in (capi.PATH_SPLIT, capi.PATH_FUSED):
+                for path in (capi.PATH_SPLIT, capi.PATH_FUSED, capi.PATH_STAGE):
                     g.set_path(path)
                     got = g.assemble_rhs(q)
                     per = [float(np.abs(got[:, v].astype(np.float64) - want[:, v]).max() / scale[v]) if scale[v] > 0 else 0.0

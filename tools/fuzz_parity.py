@@ -1,6 +1,9 @@
 """Randomised parity sweep (development aid): orders 1..7, both precisions,
-1..4 partitions, split and fused paths, random (a_old, a_new), periodic and
-walled meshes, against the CPU oracle with the tests' tolerances."""
+1..4 partitions, split, fused and stage paths, random (a_old, a_new), periodic
+and walled meshes, against the CPU oracle with the tests' tolerances. On the
+stage path (what bench.py times) a trial also takes one LSRK step through the
+one-kernel-per-stage path and compares the k register and the state with the
+oracle's Solver::step."""
 import sys
 
 import numpy as np
@@ -21,7 +24,7 @@ for trial in range(int(sys.argv[2]) if len(sys.argv) > 2 else 60):
     periodic = bool(rng.integers(0, 2))
     ranks = int(rng.integers(1, 5))
     diss = bool(rng.integers(0, 2))
-    path = [capi.PATH_SPLIT, capi.PATH_FUSED][int(rng.integers(0, 2))]
+    path = [capi.PATH_SPLIT, capi.PATH_FUSED, capi.PATH_STAGE][int(rng.integers(0, 3))]
     oc, cc = both_configs("bubble", 1 if order > 4 else int(rng.integers(1, 3)), periodic)
     so, sc = settings_pair(diss)
     go, gc = gas_pair(9.81)
@@ -39,8 +42,22 @@ for trial in range(int(sys.argv[2]) if len(sys.argv) > 2 else 60):
               for v in range(5) if scale[v] > 0)
     worst[prec] = max(worst[prec], err)
     tol = 2e-12 if prec == "f64" else 3e-5
+    extra = ""
+    if path == capi.PATH_STAGE:
+        dt = o.compute_dt(0.4)
+        dt = float(np.float32(dt)) if prec == "f32" else dt
+        o.state[:] = q
+        g.set_state(q)
+        o.step(dt)
+        g.step(dt)
+        ek = max(float(np.abs(g.get_state(capi.REG_K)[:, v].astype(np.float64) - o.kreg[:, v]).max()) / (dt * scale[v])
+                 for v in range(5) if scale[v] > 0)
+        eq = max(float(np.abs(g.get_state()[:, v].astype(np.float64) - o.state[:, v]).max()) /
+                 float(np.abs(o.state[:, v]).max()) for v in (0, 4))
+        extra = f" | step: k {ek:.2e} of dt*scale, rho/E {eq:.2e} of max|q|"
+        err = max(err, ek / 5)   # five accumulated stages
     flag = "" if err <= tol else "   <-- above tolerance"
     print(f"N={order} {prec} periodic={int(periodic)} ranks={ranks} diss={int(diss)} path={path} "
-          f"a_old={a_old:+.3f} a_new={a_new:.3f}: scaled error {err:.2e}{flag}")
+          f"a_old={a_old:+.3f} a_new={a_new:.3f}: scaled error {err:.2e}{extra}{flag}")
     n += 1
 print(f"{n} trials; worst scaled error f64 {worst['f64']:.2e}, f32 {worst['f32']:.2e}")
