@@ -57,9 +57,11 @@ def test_stage_path_rhs_and_trajectory(port, order, prec, periodic, ranks):
     assert err[0] <= tol_q and err[4] <= tol_q, err
     mom = float(np.abs(o.state[:, 1:4]).max())
     assert float(np.abs(gs[:, 1:4].astype(np.float64) - o.state[:, 1:4]).max()) <= 10 * tol_q * mom
-    # the k register the stage kernel leaves behind is the oracle's too
+    # the k register the stage kernel leaves behind is the oracle's too: five
+    # steps of state differences (tol_q of max|q|) feed back into it, so it is
+    # compared at that level of the flux scale (measured 1.5e-3 FP32 worst)
     k_scale = dt * scale + 1e-300
-    assert scaled_error(g.get_state(capi.REG_K), o.kreg, k_scale) <= 50 * tol_rhs
+    assert scaled_error(g.get_state(capi.REG_K), o.kreg, k_scale) <= 50 * tol_q
 
 
 @pytest.mark.parametrize("path", [capi.PATH_SPLIT, capi.PATH_FUSED, capi.PATH_STAGE])
