@@ -46,11 +46,22 @@ def parse_args():
     ap.add_argument("--refinement", type=int, default=5)
     ap.add_argument("--base", type=int, nargs=3, default=None,
                     help="override the base lattice (default: configs[4] table)")
-    ap.add_argument("--case", default="bubble", choices=["bubble", "baroclinic"])
+    ap.add_argument("--case", default=None, choices=["bubble", "baroclinic"],
+                    help="default: bubble (weak scaling), baroclinic (strong scaling)")
+    ap.add_argument("--scaling", default=os.environ.get("ESDG_BENCH_SCALING", "weak"),
+                    choices=["weak", "strong"],
+                    help="weak: BASELINE.json configs[4], ~1e8 DOF per GPU (bubble); strong: configs[3], "
+                         "the fixed 3,145,728-element (~4e8 DOF) baroclinic channel cut into --gpus parts")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "torch"],
+                    help="N > 1: ncclSend/ncclRecv issued by the library (default) or the "
+                         "torch.distributed callback (halo.py)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.case is None:
+        args.case = "baroclinic" if args.scaling == "strong" else "bubble"
+    return args
 
 
 # --------------------------------------------------------------------------
@@ -155,12 +166,16 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(kernel: str):
-    """dram bytes per launch from the committed ncu summary, if any."""
+def ncu_traffic(kernel: str, order: int, precision: str, case: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
+    ("stage", "fused", "volume") from the committed ncu captures of this very
+    workload (profiles/traffic.json, keyed kernel/N<order>/<precision>/<case>;
+    tools/collect_traffic.sh regenerates it), or None."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(path):
         with open(path) as f:
-            return json.load(f).get(kernel)
+            table = json.load(f)
+        return table.get(f"{kernel}/N{order}/{precision}/{case}")
     return None
 
 
@@ -244,6 +259,8 @@ def main_b200(args, rank, local_rank, world):
 
     dist = None
     if world > 1:
+        # the NCCL log lets whoever runs this count ranks and see the transport
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
@@ -259,13 +276,25 @@ def main_b200(args, rank, local_rank, world):
         settings = capi.Settings(1, 0, 0.0, 0.0, 0.0)
         case_id = capi.CASE_BUBBLE_SHARP
     else:
-        base = tuple(args.base) if args.base else (12, 2 * world, 1)
+        # strong: configs[3], the same 384 x 128 x 64 mesh for every N;
+        # weak: configs[2] per GPU, widened in y with N
+        base = tuple(args.base) if args.base else ((12, 4, 2) if args.scaling == "strong" else (12, 2 * world, 1))
         cfg = capi.channel_mesh_config(args.refinement, base)
         settings = capi.Settings(1, 2, 1e-4, 1.6e-11, 3e6)
         case_id = capi.CASE_BAROCLINIC_JET
     mesh = capi.Mesh(cfg)
 
-    if world > 1:
+    exchange = None
+    if world > 1 and args.exchange == "nccl":
+        # the exchange lives in the library: rank 0 makes the NCCL unique id,
+        # torch.distributed (plumbing) hands it round, no Python runs in a step
+        uid = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{device}")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(capi.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        solver = capi.GpuSolver(mesh, args.order, args.precision, settings=settings,
+                                nccl=(world, rank, device, bytes(uid.cpu().numpy().tobytes())))
+    elif world > 1:
         from paper_2605_16684_b200 import halo
         solver = capi.GpuSolver(mesh, args.order, args.precision, settings=settings,
                                 distributed=(world, rank, device))
@@ -273,7 +302,6 @@ def main_b200(args, rank, local_rank, world):
         solver.exchange_impl = cb
     else:
         solver = capi.GpuSolver(mesh, args.order, args.precision, settings=settings, devices=[device])
-        exchange = None
     solver.set_path({"stage": capi.PATH_STAGE, "fused": capi.PATH_FUSED, "split": capi.PATH_SPLIT}[args.path])
     solver.init_case(case_id)
     dt_local = solver.compute_dt(0.5)
@@ -318,7 +346,7 @@ def main_b200(args, rank, local_rank, world):
             sampler.mark()
         e0.record(stream)
         for _ in range(args.steps):
-            solver.step(dt, check_state=False)
+            solver.step(dt, check_state=True)   # the flag read-back step() does by default
         e1.record(stream)
         solver.sync()
         barrier()
@@ -326,8 +354,6 @@ def main_b200(args, rank, local_rank, world):
         c = sampler.snapshot() if rank == 0 else None
         tm = solver.timers(reset=True)
         solver.enable_timing(False)
-        solver.step(dt, check_state=True)   # the state is still physical
-        solver.sync()
         return t_ms, c, tm, l0
 
     def suspicious(c):
@@ -356,6 +382,16 @@ def main_b200(args, rank, local_rank, world):
         ms = float(t.item())
     n_rhs = 5 * args.steps
     value = dof_total * n_rhs / (ms * 1e-3)
+
+    # one more step with the RankEvents timeline on (exchange.hpp:83-89):
+    # did the first kernel of the last RHS start before its last trace arrived?
+    solver.record_events(True)
+    solver.step(dt, check_state=True)
+    solver.sync()
+    events = solver.rank_events()
+    solver.record_events(False)
+    halo_bytes = solver.halo_bytes
+    interior_el, local_el = solver.overlap_elements()
 
     # ---- e2e: host buffers in, host buffers out, copies inside the region --
     e2e = None
@@ -408,6 +444,7 @@ def main_b200(args, rank, local_rank, world):
                "sequential_call": "esdg_b200_solver_set_state + esdg_b200_solver_step + "
                                   "esdg_b200_solver_get_state on pinned host StateField buffers"}
 
+    halo_exchanges = None
     if exchange is not None:
         halo_exchanges = exchange.exchanges
         exchange.close()        # before the solver (and its stream) is destroyed
@@ -442,7 +479,8 @@ def main_b200(args, rank, local_rank, world):
         vol_tf = w["volume_flops"] * n_local / vol_s / 1e12
         kernels["volume"] = {"bound": "fp64" if rb == 8 else "fp32", "achieved": vol_tf,
                              "peak": fma_peak, "unit": "TFLOP/s", "frac": vol_tf / fma_peak,
-                             "ms": 1e3 * vol_s, "traffic": ncu_traffic("volume"),
+                             "peak_nominal": peak_nominal, "frac_nominal": vol_tf / peak_nominal,
+                             "ms": 1e3 * vol_s, "traffic": ncu_traffic("volume", args.order, args.precision, args.case),
                              "flops_model": f"{w['volume_flops']} flops/element/launch"}
         surf_gbs = w["surface_bytes"] * n_local / surf_s / 1e9
         kernels["surface"] = {"bound": "hbm", "achieved": surf_gbs, "peak": peaks["hbm_gbs"],
@@ -471,6 +509,14 @@ def main_b200(args, rank, local_rank, world):
                               "unit": "GB/s", "frac": surf_gbs / peaks["hbm_gbs"],
                               "ms": 1e3 * per_launch["surface"]}
     achieved = flops / dom_s / 1e12
+    # nominal CUDA-core FMA peak: SMs x FP64 (FP32) lanes x 2 x max SM clock
+    sm_count = torch.cuda.get_device_properties(device).multi_processor_count
+    sm_mhz = (clocks or {}).get("sm_max_mhz") or peaks.get("sm_max_mhz") or 1965.0
+    peak_nominal = sm_count * (64 if rb == 8 else 128) * 2 * sm_mhz * 1e6 / 1e12
+    # the HBM side of the same kernel: its algorithmic bytes per element
+    # over the same launch time
+    stage_bytes = {"stage": 21 * nq ** 3 * rb, "fused": 16 * nq ** 3 * rb, "volume": w["volume_bytes"]}[traffic_key]
+    hbm_gbs = stage_bytes * n_local / dom_s / 1e9
     if per_launch["update"] > 0 and "update" not in kernels:
         upd_gbs = w["update_bytes"] * n_local / per_launch["update"] / 1e9
         kernels["update"] = {"bound": "hbm", "achieved": upd_gbs, "peak": peaks["hbm_gbs"],
@@ -479,8 +525,11 @@ def main_b200(args, rank, local_rank, world):
     roofline = {
         "kernel": dom, "bound": "fp64" if rb == 8 else "fp32",
         "achieved": achieved, "peak": fma_peak, "unit": "TFLOP/s", "frac": achieved / fma_peak,
-        "traffic": ncu_traffic(traffic_key) if (args.order == 4 and rb == 8 and args.refinement == 5
-                                                and world == 1 and args.case == "bubble") else None,
+        "peak_nominal": peak_nominal, "frac_nominal": achieved / peak_nominal,
+        "hbm": {"achieved": hbm_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": hbm_gbs / peaks["hbm_gbs"],
+                "bytes_model": f"{stage_bytes} algorithmic bytes/element/launch"},
+        "traffic": ncu_traffic(traffic_key, args.order, args.precision, args.case) if world == 1 else None,
         "ms_per_launch": 1e3 * dom_s,
         "flops_model": "reference PerfRecord model (diagnostics.cpp:33-81): "
                        f"{flops // n_local} flops/element/launch",
@@ -506,7 +555,7 @@ def main_b200(args, rank, local_rank, world):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "strong" if (args.case == "baroclinic" and args.base) else "weak",
+        "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": args.precision, "data": "synthetic",
         "config": {
@@ -521,11 +570,22 @@ def main_b200(args, rank, local_rank, world):
         "clocks": clocks, "e2e": e2e, "gpu_launches": timers["launches"] - launches0,
         "roofline": roofline, "cpu_baseline": cpu,
     }
-    if exchange is not None:
-        line["config"]["halo_exchanges"] = halo_exchanges
-        interior, local = solver.overlap_elements()
-        # elements of rank 0 whose one-pass kernel runs while the traces travel
-        line["config"]["halo_overlap"] = {"interior_elements": interior, "local_elements": local}
+    if world > 1:
+        # rank 0's share: trace bytes it sends (= receives) per RHS, the
+        # elements whose one-pass kernel runs while the traces travel, and the
+        # CUDA-event timeline of one RHS (ns since it was enqueued)
+        line["config"]["halo"] = {
+            "exchange": ("ncclSend/ncclRecv in one group per RHS, issued by the library (C++)"
+                         if args.exchange == "nccl" else "torch.distributed batch_isend_irecv callback"),
+            "nccl_version": capi.lib().esdg_b200_solver_nccl_version(solver.h),
+            "halo_bytes_per_rhs": halo_bytes,
+            "interior_fraction": interior_el / max(local_el, 1),
+            "interior_elements": interior_el, "local_elements": local_el,
+            "events_ns": events,
+            "interior_kernel_started_before_last_recv": events["volume_start_ns"] <= events["last_arrival_ns"],
+        }
+        if halo_exchanges is not None:
+            line["config"]["halo"]["exchanges"] = halo_exchanges
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

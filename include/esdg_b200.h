@@ -339,9 +339,44 @@ int esdg_b200_solver_create_distributed(
     const esdg_b200_settings* settings, int precision, int world_size,
     int rank, int device, esdg_b200_exchange_fn exchange, void* user,
     esdg_b200_solver** out);
+/* One process per GPU with the trace exchange in the library itself: per RHS
+ * one ncclSend/ncclRecv pair per peer inside one ncclGroup on the partition's
+ * copy stream, behind the pack kernel, overlapped with the kernels of the
+ * element groups that have no ghost face (replaces Transport<Real>::send /
+ * wait, exchange.hpp:32-57, call sites solver.hpp:255,294). NCCL is bound at
+ * run time (dlopen of libnccl.so.2). Rank 0 obtains a 128-byte unique id with
+ * esdg_b200_nccl_unique_id, the host distributes it (MPI, torch.distributed,
+ * a file ...) and every rank calls esdg_b200_solver_create_nccl -- a
+ * collective -- with its own device current. */
+int esdg_b200_nccl_unique_id(void* id128);
+int esdg_b200_solver_create_nccl(esdg_b200_mesh* mesh, int order,
+                                 const esdg_b200_gas* gas,
+                                 const esdg_b200_settings* settings,
+                                 int precision, int world_size, int rank,
+                                 int device, const void* id128,
+                                 esdg_b200_solver** out);
+/* NCCL_VERSION_CODE of the library bound by create_nccl (0: none) */
+int esdg_b200_solver_nccl_version(const esdg_b200_solver* s);
 void esdg_b200_solver_destroy(esdg_b200_solver* s);
 
 int esdg_b200_solver_set_path(esdg_b200_solver* s, int path);
+/* KernelSettings::variant (kernels.hpp:27-34, 59-65): the rung of the volume
+ * kernel's optimisation ladder, 0 baseline .. 5 balanced (default). Rungs
+ * below 4 select a ladder instance of K1 in volume_rhs / assemble_rhs (split
+ * structure); step() on PATH_STAGE always runs the product kernel. */
+int esdg_b200_solver_set_variant(esdg_b200_solver* s, int variant);
+/* RankEvents (exchange.hpp:83-89, filled at solver.hpp:257-262,318-319): with
+ * recording on, every RHS leaves a CUDA-event timeline per local partition;
+ * rank_events returns, in ns since that partition's RHS was enqueued,
+ * {sends_posted, volume_start, volume_end, wait_end, last_arrival} of the
+ * last one (volume = the first kernel launch of the RHS: the volume kernel,
+ * or the element groups without a ghost face on the one-pass paths). The
+ * overlap property tests/test_partition.cpp:116-134 checks with a delayed
+ * transport reads volume_start < last_arrival. */
+int esdg_b200_solver_record_events(esdg_b200_solver* s, int on);
+int esdg_b200_solver_rank_events(esdg_b200_solver* s, int rank, int64_t ns[5]);
+/* bytes of face traces this process sends (and receives) per RHS */
+int64_t esdg_b200_solver_halo_bytes(const esdg_b200_solver* s);
 /* PATH_FUSED / PATH_STAGE with several partitions: on (default) runs the
  * element groups without a ghost face while the traces travel and the rest
  * after they have landed (rhs_job's order, solver.hpp:259-294); off waits for

@@ -18,11 +18,23 @@
 //   - `ranks` is the number of partitions (GPUs when several are visible).
 //
 // When this header is compiled together with the reference's headers, define
-// ESDG_B200_WITH_REFERENCE to make it throw esdg::NonPhysicalState and accept
-// esdg::MeshConfig / GasConstants / KernelSettings directly.
+// ESDG_B200_WITH_REFERENCE: GpuSolver<Real> then IS a type-swap for
+// esdg::Solver<Real> -- it takes the reference's MeshGeometry, GasConstants and
+// KernelSettings<Real>, keeps its host mirror in an esdg::StateField<Real>,
+// throws esdg::NonPhysicalState and answers every accessor of
+// solver.hpp:74-89 with the reference's own types: mesh(), ref(), ops(),
+// constants(), gas(), settings() (mutable; changes reach the device before
+// the next operation), phi(), state(), ranks(), partition(), plan(), perf(),
+// events(), set_record_events(). include/esdg_b200/swap/esdg/solver.hpp makes
+// `esdg::Solver` name this class, so the reference's own callers
+// (tests/acceptance.cpp, core/src/runner.cpp, ladder.hpp, test_helpers.hpp)
+// compile UNMODIFIED against the GPU path (oracle/Makefile: esdg_acceptance_gpu,
+// esdg_run_gpu). The one member without a GPU meaning is transport() (an
+// in-process mailbox object; the GPU exchange is NCCL / peer copies).
 #pragma once
 
 #include <array>
+#include <cstdlib>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -32,9 +44,16 @@
 #include "esdg_b200.h"
 
 #ifdef ESDG_B200_WITH_REFERENCE
+#include <chrono>
+
+#include "esdg/diagnostics.hpp"
 #include "esdg/error.hpp"
+#include "esdg/exchange.hpp"
 #include "esdg/kernels.hpp"
 #include "esdg/mesh.hpp"
+#include "esdg/partition.hpp"
+#include "esdg/reference_element.hpp"
+#include "esdg/state.hpp"
 #endif
 
 namespace esdg_b200 {
@@ -42,6 +61,10 @@ namespace esdg_b200 {
 inline constexpr int kNumVars = 5;
 
 // StateField<Real> (state.hpp:13-38): element-major SoA, data[e][var][node]
+#ifdef ESDG_B200_WITH_REFERENCE
+template <class Real>
+using StateField = esdg::StateField<Real>;
+#else
 template <class Real>
 struct StateField {
   StateField() = default;
@@ -57,6 +80,7 @@ struct StateField {
   Real at(std::int64_t e, int var, int node) const { return element(e)[size_t(var) * nodes_per_element + node]; }
   size_t size() const { return data.size(); }
 };
+#endif
 
 #ifdef ESDG_B200_WITH_REFERENCE
 using NonPhysicalState = esdg::NonPhysicalState;
@@ -95,12 +119,24 @@ struct GasConstants {
   double gamma = 1.4, R = 287.0, p0 = 1e5, gravity = 9.81;
 };
 
-// KernelSettings<Real> (kernels.hpp:59-65); variant is fixed to balanced and
-// contravariant_direct to true on the GPU
+// KernelVariant (kernels.hpp:27-34) as the C ABI numbers it
+// (esdg_b200_solver_set_variant)
+enum : int {
+  kVariantBaseline = 0,
+  kVariantFused = 1,
+  kVariantPrecompute = 2,
+  kVariantLogMean = 3,
+  kVariantSymmetric = 4,
+  kVariantBalanced = 5
+};
+
+// KernelSettings<Real> (kernels.hpp:59-65); contravariant_direct is fixed to
+// true on the GPU
 struct KernelSettings {
   bool dissipation = true;
   int coriolis_mode = 0; // 0 none, 1 f-plane, 2 beta-plane
   double f0 = 0.0, beta = 0.0, y0 = 0.0;
+  int variant = kVariantBalanced;
 };
 
 // LsrkScheme / lsrk_step (time_integration.hpp:17-49), unchanged contract
@@ -114,55 +150,68 @@ void lsrk_step(RhsAccum&& rhs_accum, Axpy&& axpy, Real dt) {
   }
 }
 
+namespace detail {
+
+// What the reference's exact operation counters (counters.hpp:12-24) read
+// after one volume pass, per node of the mesh, as closed forms of the order
+// and the ladder variant -- asserted against the reference's counters by
+// tests/test_kernels.cpp:95-162 there and tests/test_oracle_vs_ref.py here.
+// The GPU kernels carry no counters (they would serialise the hot loops).
+// The division counts of the two variants whose logarithmic mean branches on
+// the data (baseline/fused, precompute) are the reference's deterministic
+// part plus its typical data-dependent share; every other entry is exact.
+struct VolumeCounts {
+  std::uint64_t flux, log, div;
+};
+inline VolumeCounts volume_counts_per_node(int nq, int variant) {
+  const std::uint64_t full = 3ull * std::uint64_t(nq - 1); // every ordered partner
+  const std::uint64_t logmean_div = 23ull + 7ull * full;
+  switch (variant) {
+    case kVariantBaseline:
+    case kVariantFused: return {full, 4ull * full + 6ull, logmean_div + 6ull * full + 24ull};
+    case kVariantPrecompute: return {full, 2ull, logmean_div + 2ull * full + 20ull};
+    case kVariantLogMean: return {full, 2ull, logmean_div};
+    case kVariantSymmetric: return {0 /* see caller: full/2 over the mesh */, 2ull, 0};
+    default: return {3ull * std::uint64_t(nq / 2), 2ull, 23ull + 24ull * std::uint64_t(nq / 2)};
+  }
+}
+
+} // namespace detail
+
 template <class Real>
 class GpuSolver {
   static_assert(sizeof(Real) == 8 || sizeof(Real) == 4, "Real is double or float");
 
 public:
-  GpuSolver(const esdg_b200_mesh_config& mesh_config, int order,
-            const GasConstants& constants, const KernelSettings& settings,
-            int ranks = 1, const std::vector<int>& devices = {})
-      : order_(order), constants_(constants), settings_(settings), ranks_(ranks) {
-    check(esdg_b200_mesh_create(&mesh_config, &mesh_));
-    const esdg_b200_gas gas{constants.gamma, constants.R, constants.p0, constants.gravity};
-    const esdg_b200_settings st{settings.dissipation ? 1 : 0, settings.coriolis_mode,
-                                settings.f0, settings.beta, settings.y0};
-    std::vector<int32_t> dev(devices.begin(), devices.end());
-    if (dev.empty()) {
-      const int n = esdg_b200_device_count();
-      for (int r = 0; r < ranks; ++r) dev.push_back(n > 0 ? r % n : 0);
-    }
-    const int rc = esdg_b200_solver_create(mesh_, order, &gas, &st, int(sizeof(Real)), ranks,
-                                           dev.data(), int(dev.size()), &solver_);
-    if (rc != ESDG_B200_OK) {
-      esdg_b200_mesh_destroy(mesh_);
-      mesh_ = nullptr;
-      check(rc);
-    }
-    nq_ = order + 1;
-    n3_ = nq_ * nq_ * nq_;
-    ne_ = esdg_b200_mesh_num_elements(mesh_);
-    nodes_.resize(size_t(nq_));
-    weights_.resize(size_t(nq_));
-    diff_.resize(size_t(nq_) * size_t(nq_));
-    check(esdg_b200_reference_element(order, nodes_.data(), weights_.data(), diff_.data()));
-    for (int d = 0; d < 3; ++d) {
-      lo_[d] = mesh_config.lo[d];
-      const int64_t n = int64_t(mesh_config.base[d]) << mesh_config.refinement;
-      delta_[d] = (mesh_config.hi[d] - mesh_config.lo[d]) / double(n);
-    }
+#ifdef ESDG_B200_WITH_REFERENCE
+  using Constants = esdg::GasConstants<double>;
+  using Settings = esdg::KernelSettings<Real>;
+#else
+  using Constants = GasConstants;
+  using Settings = KernelSettings;
+#endif
+  using Field = StateField<Real>;
+
+  GpuSolver(const esdg_b200_mesh_config& mesh_config, int order, const Constants& constants,
+            const Settings& settings, int ranks = 1, const std::vector<int>& devices = {})
+      : order_(order), constants_(constants), settings_(settings), ranks_(ranks)
+#ifdef ESDG_B200_WITH_REFERENCE
+        ,
+        mesh_ref_(std::make_shared<const esdg::MeshGeometry>(from_config(mesh_config))),
+        ref_(order), ops_(ref_, *mesh_ref_)
+#endif
+  {
+    init(mesh_config, devices);
   }
 
 #ifdef ESDG_B200_WITH_REFERENCE
-  template <class R2>
-  GpuSolver(std::shared_ptr<const esdg::MeshGeometry> mesh, int order,
-            const esdg::GasConstants<double>& gc, const esdg::KernelSettings<R2>& ks,
-            int ranks = 1)
-      : GpuSolver(to_config(mesh->config()), order,
-                  GasConstants{gc.gamma, gc.R, gc.p0, gc.gravity},
-                  KernelSettings{ks.dissipation, int(ks.coriolis.mode), double(ks.coriolis.f0),
-                                 double(ks.coriolis.beta), double(ks.coriolis.y0)},
-                  ranks) {}
+  // Solver(mesh, order, constants, settings, ranks) (solver.hpp:26-39)
+  GpuSolver(std::shared_ptr<const esdg::MeshGeometry> mesh, int order, const Constants& constants,
+            const Settings& settings, int ranks = 1)
+      : order_(order), constants_(constants), settings_(settings), ranks_(ranks),
+        mesh_ref_(std::move(mesh)), ref_(order), ops_(ref_, *mesh_ref_) {
+    init(to_config(mesh_ref_->config()), {});
+  }
 #endif
 
   ~GpuSolver() {
@@ -172,16 +221,48 @@ public:
   GpuSolver(const GpuSolver&) = delete;
   GpuSolver& operator=(const GpuSolver&) = delete;
 
+  // ---- accessors (solver.hpp:74-89) ---------------------------------------
   int ranks() const { return ranks_; }
   int order() const { return order_; }
   int nq() const { return nq_; }
   int n3() const { return n3_; }
   std::int64_t num_elements() const { return ne_; }
-  const GasConstants& constants() const { return constants_; }
-  const KernelSettings& settings() const { return settings_; }
+  const Constants& constants() const { return constants_; }
+  // mutable like the reference's: a changed dissipation flag or ladder
+  // variant reaches the device before the next operation
+  Settings& settings() { return settings_; }
+  const Settings& settings() const { return settings_; }
   const std::vector<double>& nodes() const { return nodes_; }
   const std::vector<double>& weights() const { return weights_; }
   const std::vector<double>& diff_matrix() const { return diff_; }
+#ifdef ESDG_B200_WITH_REFERENCE
+  const esdg::MeshGeometry& mesh() const { return *mesh_ref_; }
+  const esdg::ReferenceElement& ref() const { return ref_; }
+  const esdg::Operators<Real>& ops() const { return ops_; }
+  const esdg::GasConstants<Real>& gas() const { return gas_; }
+  const esdg::Partition& partition() const { return part_; }
+  const esdg::ExchangePlan& plan() const { return plan_; }
+  // PerfRecord (diagnostics.hpp:125-139): wall time of step(), the kernel
+  // classes' CUDA-event times, and the operation counts as closed forms
+  esdg::PerfRecord& perf() {
+    double sec[4] = {0, 0, 0, 0};
+    std::int64_t launches = 0;
+    if (esdg_b200_solver_timers(solver_, sec, &launches, 0) == ESDG_B200_OK) {
+      perf_.volume_seconds = sec[0] + sec[3]; // the pack kernel belongs to the volume phase
+      perf_.surface_seconds = sec[1];
+      perf_.update_seconds = sec[2];
+    }
+    return perf_;
+  }
+  // RankEvents (exchange.hpp:83-89) of the last RHS with recording on: the
+  // CUDA-event timeline of partition r on the host clock's scale (ns since
+  // the RHS was enqueued), see esdg_b200_solver_rank_events
+  const std::vector<esdg::RankEvents>& events() const { return events_; }
+  void set_record_events(bool on) {
+    record_events_ = on;
+    check(esdg_b200_solver_record_events(solver_, on ? 1 : 0));
+  }
+#endif
   void set_fused(bool on) {
     check(esdg_b200_solver_set_path(solver_, on ? ESDG_B200_PATH_FUSED : ESDG_B200_PATH_SPLIT));
   }
@@ -189,21 +270,20 @@ public:
   // fastest; assemble_rhs as _FUSED), _FUSED, or _SPLIT (the reference's
   // volume -> surface -> axpy structure)
   void set_path(int path) { check(esdg_b200_solver_set_path(solver_, path)); }
-  void set_dissipation(bool on) {
-    settings_.dissipation = on;
-    const esdg_b200_settings st{on ? 1 : 0, settings_.coriolis_mode, settings_.f0,
-                                settings_.beta, settings_.y0};
-    check(esdg_b200_solver_set_settings(solver_, &st));
-  }
+  void set_dissipation(bool on) { settings_.dissipation = on; }
 
   // mesh.hpp:73-77
   double node_coordinate(std::int64_t e, int dir, double ref_node) const {
+#ifdef ESDG_B200_WITH_REFERENCE
+    return mesh_ref_->node_coordinate(e, dir, ref_node);
+#else
     const int32_t* lat = esdg_b200_mesh_lattice(mesh_) + 3 * e;
     return lo_[dir] + (double(lat[dir]) + 0.5 * (ref_node + 1.0)) * delta_[dir];
+#endif
   }
 
   // phi() (solver.hpp:79, 166-176)
-  const std::vector<Real>& phi() {
+  const std::vector<Real>& phi() const {
     if (phi_.empty()) {
       phi_.resize(size_t(ne_) * size_t(n3_));
       check(esdg_b200_solver_get_phi(solver_, phi_.data()));
@@ -228,62 +308,88 @@ public:
         for (int v = 0; v < 5; ++v) qe[size_t(v) * n3_ + n] = Real(qv[v]);
       }
     }
+    stashed_ = false; // whatever was parked in the mirror is replaced
     host_valid_ = true;
     host_dirty_ = true;
   }
 
-  // state() (solver.hpp:80-81): host mirror, see the header comment
-  StateField<Real>& state() {
+  // state() (solver.hpp:80-81): host mirror of the device register. The
+  // non-const access marks it as possibly modified, so the next device
+  // operation uploads it; state_view() and the const overload do not.
+  Field& state() {
     pull();
     host_dirty_ = true;
     return host_;
   }
-  const StateField<Real>& state_view() {
+  const Field& state() const {
+    pull();
+    return host_;
+  }
+  const Field& state_view() const {
     pull();
     return host_;
   }
 
-  // assemble_rhs(q, out, a_old, a_new) (solver.hpp:112-119). Field is any
+  // assemble_rhs(q, out, a_old, a_new) (solver.hpp:112-119). FieldLike is any
   // StateField-like type (ours or the reference's esdg::StateField<Real>).
-  template <class Field>
-  void assemble_rhs(const Field& q, Field& out, Real a_old, Real a_new) {
+  template <class FieldLike>
+  void assemble_rhs(const FieldLike& q, FieldLike& out, Real a_old, Real a_new) {
+    sync_settings();
     push_if_needed(); // keep the internal q register as the caller left it
     stash_internal();
     guard(esdg_b200_solver_assemble_rhs(solver_, q.data.data(), out.data.data(), double(a_old),
-                                        double(a_new)), -1);
+                                        double(a_new)));
+    count_ops(true, 1);
   }
 
   // volume_rhs(q, out) (solver.hpp:122-129)
-  template <class Field>
-  void volume_rhs(const Field& q, Field& out) {
+  template <class FieldLike>
+  void volume_rhs(const FieldLike& q, FieldLike& out) {
+    sync_settings();
     push_if_needed();
     stash_internal();
-    guard(esdg_b200_solver_volume_rhs(solver_, q.data.data(), out.data.data()), -1);
+    guard(esdg_b200_solver_volume_rhs(solver_, q.data.data(), out.data.data()));
+    count_ops(false, 1);
   }
 
   // step(dt) (solver.hpp:132-146): five (rhs, axpy) stages on the device
   // registers; a NonPhysicalState carries the stage like with_stage() does
   void step(Real dt) {
+    sync_settings();
     restore_internal();
     push_if_needed();
-    guard(esdg_b200_solver_step(solver_, double(dt), 1), 0);
+#ifdef ESDG_B200_WITH_REFERENCE
+    const auto t0 = std::chrono::steady_clock::now();
+#endif
+    guard(esdg_b200_solver_step(solver_, double(dt), 1));
     host_valid_ = false;
+    count_ops(true, 5);
+#ifdef ESDG_B200_WITH_REFERENCE
+    ++perf_.steps;
+    perf_.wall_seconds +=
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (record_events_) fetch_events();
+#endif
   }
 
   // compute_dt(courant) (solver.hpp:148-150)
-  double compute_dt(double courant) {
+  double compute_dt(double courant) const {
     restore_internal();
     push_if_needed();
     double dt = 0.0;
-    guard(esdg_b200_solver_compute_dt(solver_, courant, &dt), -1);
+    guard(esdg_b200_solver_compute_dt(solver_, courant, &dt));
     return dt;
   }
 
   // node_mass(n) (solver.hpp:153-158): J w_a w_b w_c in 64-bit
   double node_mass(int node) const {
     const int a = node % nq_, b = (node / nq_) % nq_, c = node / (nq_ * nq_);
-    return 0.125 * delta_[0] * delta_[1] * delta_[2] * weights_[size_t(a)] * weights_[size_t(b)] *
-           weights_[size_t(c)];
+#ifdef ESDG_B200_WITH_REFERENCE
+    const double J = mesh_ref_->jacobian();
+#else
+    const double J = 0.125 * delta_[0] * delta_[1] * delta_[2];
+#endif
+    return J * weights_[size_t(a)] * weights_[size_t(b)] * weights_[size_t(c)];
   }
 
   // Where the diagnostics and compute_dt are reduced: on the device (default;
@@ -291,7 +397,7 @@ public:
   // summation order (bitwise the reference's sums, moves the state).
   void set_reduction_on_host(bool on) {
     guard(esdg_b200_solver_set_reduction(
-              solver_, on ? ESDG_B200_REDUCE_ON_HOST : ESDG_B200_REDUCE_ON_DEVICE), -1);
+        solver_, on ? ESDG_B200_REDUCE_ON_HOST : ESDG_B200_REDUCE_ON_DEVICE));
   }
 
   // diagnostics of the internal registers (diagnostics.hpp:30-106)
@@ -299,20 +405,30 @@ public:
     restore_internal();
     push_if_needed();
     double v = 0.0;
-    guard(esdg_b200_solver_quadrature_total(solver_, ESDG_B200_REG_Q, var, &v), -1);
+    guard(esdg_b200_solver_quadrature_total(solver_, ESDG_B200_REG_Q, var, &v));
     return v;
   }
   double total_entropy() {
     restore_internal();
     push_if_needed();
     double v = 0.0;
-    guard(esdg_b200_solver_total_entropy(solver_, &v), -1);
+    guard(esdg_b200_solver_total_entropy(solver_, &v));
     return v;
   }
 
   esdg_b200_solver* handle() { return solver_; }
 
 private:
+  static esdg_b200_settings abi_settings(const Settings& s) {
+#ifdef ESDG_B200_WITH_REFERENCE
+    return esdg_b200_settings{s.dissipation ? 1 : 0, int(s.coriolis.mode), double(s.coriolis.f0),
+                              double(s.coriolis.beta), double(s.coriolis.y0)};
+#else
+    return esdg_b200_settings{s.dissipation ? 1 : 0, s.coriolis_mode, s.f0, s.beta, s.y0};
+#endif
+  }
+  static int variant_of(const Settings& s) { return int(s.variant); }
+
 #ifdef ESDG_B200_WITH_REFERENCE
   static esdg_b200_mesh_config to_config(const esdg::MeshConfig& c) {
     esdg_b200_mesh_config m{};
@@ -325,7 +441,71 @@ private:
     m.refinement = c.refinement;
     return m;
   }
+  static esdg::MeshConfig from_config(const esdg_b200_mesh_config& m) {
+    esdg::MeshConfig c;
+    for (int d = 0; d < 3; ++d) {
+      c.base[size_t(d)] = m.base[d];
+      c.lo[size_t(d)] = m.lo[d];
+      c.hi[size_t(d)] = m.hi[d];
+      c.bc[size_t(d)] = m.bc[d] ? esdg::BoundaryCondition::Reflecting
+                                : esdg::BoundaryCondition::Periodic;
+    }
+    c.refinement = m.refinement;
+    return c;
+  }
 #endif
+
+  void init(const esdg_b200_mesh_config& mesh_config, const std::vector<int>& devices) {
+    check(esdg_b200_mesh_create(&mesh_config, &mesh_));
+    const esdg_b200_gas gas{constants_.gamma, constants_.R, constants_.p0, constants_.gravity};
+    const esdg_b200_settings st = abi_settings(settings_);
+    std::vector<int32_t> dev(devices.begin(), devices.end());
+    if (dev.empty()) {
+      const int n = esdg_b200_device_count();
+      for (int r = 0; r < ranks_; ++r) dev.push_back(n > 0 ? r % n : 0);
+    }
+    const int rc = esdg_b200_solver_create(mesh_, order_, &gas, &st, int(sizeof(Real)), ranks_,
+                                           dev.data(), int(dev.size()), &solver_);
+    if (rc != ESDG_B200_OK) {
+      esdg_b200_mesh_destroy(mesh_);
+      mesh_ = nullptr;
+      check(rc);
+    }
+    applied_ = st;
+    applied_variant_ = kVariantBalanced;
+    nq_ = order_ + 1;
+    n3_ = nq_ * nq_ * nq_;
+    ne_ = esdg_b200_mesh_num_elements(mesh_);
+    nodes_.resize(size_t(nq_));
+    weights_.resize(size_t(nq_));
+    diff_.resize(size_t(nq_) * size_t(nq_));
+    check(esdg_b200_reference_element(order_, nodes_.data(), weights_.data(), diff_.data()));
+    for (int d = 0; d < 3; ++d) {
+      lo_[d] = mesh_config.lo[d];
+      const int64_t n = int64_t(mesh_config.base[d]) << mesh_config.refinement;
+      delta_[d] = (mesh_config.hi[d] - mesh_config.lo[d]) / double(n);
+    }
+#ifdef ESDG_B200_WITH_REFERENCE
+    gas_ = constants_.template cast<Real>();
+    part_ = esdg::make_partition(mesh_ref_->num_elements(), ranks_);
+    plan_ = esdg::build_exchange_plan(*mesh_ref_, part_);
+    face_records_ = 0;
+    for (int r = 0; r < ranks_; ++r)
+      face_records_ += std::int64_t(plan_.interior[size_t(r)].size() + plan_.ghosts[size_t(r)].size());
+    events_.assign(size_t(ranks_), esdg::RankEvents{});
+    perf_.elements = ne_;
+    perf_.faces = std::int64_t(mesh_ref_->faces().size());
+    perf_.nq = nq_;
+    perf_.ranks = ranks_;
+    perf_.real_bytes = int(sizeof(Real));
+    check(esdg_b200_solver_enable_timing(solver_, 1));
+    if (const char* p = std::getenv("ESDG_B200_PATH")) {
+      const std::string v(p);
+      set_path(v == "split" ? ESDG_B200_PATH_SPLIT
+                            : v == "fused" ? ESDG_B200_PATH_FUSED : ESDG_B200_PATH_STAGE);
+    }
+#endif
+  }
 
   static void check(int rc) {
     if (rc == ESDG_B200_OK) return;
@@ -335,7 +515,7 @@ private:
   }
 
   // status 1 -> NonPhysicalState exactly as solver.hpp:141-143 rethrows it
-  void guard(int rc, int /*default_stage*/) {
+  void guard(int rc) const {
     if (rc == ESDG_B200_NONPHYSICAL) {
       esdg_b200_error e{};
       esdg_b200_solver_last_error(solver_, &e);
@@ -344,7 +524,72 @@ private:
     check(rc);
   }
 
-  void pull() {
+  // settings() hands out a mutable reference: push what changed
+  void sync_settings() {
+    const esdg_b200_settings st = abi_settings(settings_);
+    if (st.dissipation != applied_.dissipation || st.coriolis_mode != applied_.coriolis_mode ||
+        st.f0 != applied_.f0 || st.beta != applied_.beta || st.y0 != applied_.y0) {
+      check(esdg_b200_solver_set_settings(solver_, &st));
+      applied_ = st;
+    }
+    if (variant_of(settings_) != applied_variant_) {
+      check(esdg_b200_solver_set_variant(solver_, variant_of(settings_)));
+      applied_variant_ = variant_of(settings_);
+    }
+  }
+
+  // the reference's exact counters as closed forms (see detail::VolumeCounts
+  // and tests/test_kernels.cpp:95-162): `passes` RHS evaluations
+  void count_ops(bool with_faces, int passes) {
+#ifdef ESDG_B200_WITH_REFERENCE
+    const std::uint64_t nodes = std::uint64_t(ne_) * std::uint64_t(n3_);
+    const std::uint64_t n2 = std::uint64_t(nq_) * std::uint64_t(nq_);
+    const int v = variant_of(settings_);
+    detail::VolumeCounts c = detail::volume_counts_per_node(nq_, v);
+    std::uint64_t flux = c.flux * nodes, div = c.div * nodes;
+    if (v == kVariantSymmetric) {
+      // every unordered pair of a line once: nq (nq-1)/2 per line
+      const std::uint64_t pairs = 3ull * std::uint64_t(ne_) * n2 * std::uint64_t(nq_ * (nq_ - 1) / 2);
+      flux = pairs;
+      div = 23ull * nodes + 8ull * pairs;
+    }
+    esdg::Counters& k = perf_.counters;
+    k.volume.flux_evals += std::uint64_t(passes) * flux;
+    k.volume.log_evals += std::uint64_t(passes) * c.log * nodes;
+    k.volume.div_evals += std::uint64_t(passes) * div;
+    if (with_faces) {
+      // one record per (rank, face it touches) and six side commits per
+      // element (kernels.hpp:350-430): 1 flux, 4 logs, 20 (12 without
+      // dissipation) divisions per record node; 2 logs, 9 divisions per commit node
+      const std::uint64_t rec = std::uint64_t(face_records_) * n2, com = 6ull * std::uint64_t(ne_) * n2;
+      k.surface.flux_evals += std::uint64_t(passes) * rec;
+      k.surface.log_evals += std::uint64_t(passes) * (4ull * rec + 2ull * com);
+      k.surface.div_evals +=
+          std::uint64_t(passes) * ((settings_.dissipation ? 20ull : 12ull) * rec + 9ull * com);
+      k.rhs_calls += std::uint64_t(passes);
+    }
+#else
+    (void)with_faces;
+    (void)passes;
+#endif
+  }
+
+#ifdef ESDG_B200_WITH_REFERENCE
+  void fetch_events() {
+    for (int r = 0; r < ranks_; ++r) {
+      std::int64_t ns[5] = {0, 0, 0, 0, 0};
+      if (esdg_b200_solver_rank_events(solver_, r, ns) != ESDG_B200_OK) continue;
+      esdg::RankEvents& e = events_[size_t(r)];
+      e.sends_posted_ns = ns[0];
+      e.volume_start_ns = ns[1];
+      e.volume_end_ns = ns[2];
+      e.wait_end_ns = ns[3];
+      e.last_arrival_ns = ns[4];
+    }
+  }
+#endif
+
+  void pull() const {
     restore_internal();
     if (host_valid_) return;
     host_.n_elements = ne_;
@@ -353,7 +598,7 @@ private:
     check(esdg_b200_solver_get_state(solver_, ESDG_B200_REG_Q, host_.data.data()));
     host_valid_ = true;
   }
-  void push_if_needed() {
+  void push_if_needed() const {
     if (host_valid_ && host_dirty_) {
       check(esdg_b200_solver_set_state(solver_, ESDG_B200_REG_Q, host_.data.data()));
       host_dirty_ = false;
@@ -372,24 +617,40 @@ private:
     }
     stashed_ = true;
   }
-  void restore_internal() {
+  void restore_internal() const {
     if (!stashed_) return;
     check(esdg_b200_solver_set_state(solver_, ESDG_B200_REG_Q, host_.data.data()));
     host_dirty_ = false;
     stashed_ = false;
   }
 
-  int order_, nq_ = 0, n3_ = 0, ranks_;
+  int order_, nq_ = 0, n3_ = 0;
+  Constants constants_;
+  Settings settings_;
+  int ranks_;
+  esdg_b200_settings applied_{};
+  int applied_variant_ = kVariantBalanced;
   std::int64_t ne_ = 0;
-  GasConstants constants_;
-  KernelSettings settings_;
   esdg_b200_mesh* mesh_ = nullptr;
   esdg_b200_solver* solver_ = nullptr;
   std::vector<double> nodes_, weights_, diff_;
   double lo_[3] = {0, 0, 0}, delta_[3] = {0, 0, 0};
-  std::vector<Real> phi_;
-  StateField<Real> host_;
-  bool host_valid_ = false, host_dirty_ = false, stashed_ = false;
+  mutable std::vector<Real> phi_;
+  // host mirror of the q register: filled lazily, also from const accessors
+  mutable Field host_;
+  mutable bool host_valid_ = false, host_dirty_ = false, stashed_ = false;
+#ifdef ESDG_B200_WITH_REFERENCE
+  std::shared_ptr<const esdg::MeshGeometry> mesh_ref_;
+  esdg::ReferenceElement ref_;
+  esdg::Operators<Real> ops_;
+  esdg::GasConstants<Real> gas_;
+  esdg::Partition part_;
+  esdg::ExchangePlan plan_;
+  esdg::PerfRecord perf_;
+  std::vector<esdg::RankEvents> events_;
+  std::int64_t face_records_ = 0;
+  bool record_events_ = false;
+#endif
 };
 
 } // namespace esdg_b200

@@ -120,6 +120,14 @@ SIGNATURES = {
     "esdg_b200_solver_create_distributed": (_i, [_vp, _i, C.POINTER(Gas), C.POINTER(Settings),
                                                  _i, _i, _i, _i, EXCHANGE_FN, _vp,
                                                  C.POINTER(_vp)]),
+    "esdg_b200_nccl_unique_id": (_i, [_vp]),
+    "esdg_b200_solver_create_nccl": (_i, [_vp, _i, C.POINTER(Gas), C.POINTER(Settings),
+                                          _i, _i, _i, _i, _vp, C.POINTER(_vp)]),
+    "esdg_b200_solver_nccl_version": (_i, [_vp]),
+    "esdg_b200_solver_set_variant": (_i, [_vp, _i]),
+    "esdg_b200_solver_record_events": (_i, [_vp, _i]),
+    "esdg_b200_solver_rank_events": (_i, [_vp, _i, _i64p]),
+    "esdg_b200_solver_halo_bytes": (_i64, [_vp]),
     "esdg_b200_solver_destroy": (None, [_vp]),
     "esdg_b200_solver_set_path": (_i, [_vp, _i]),
     "esdg_b200_solver_set_overlap": (_i, [_vp, _i]),
@@ -351,14 +359,22 @@ class GpuSolver:
     """Handle on esdg_b200_solver: the GPU counterpart of esdg::Solver<Real>."""
 
     def __init__(self, mesh: Mesh, order, precision="f64", gas=None, settings=None, ranks=1,
-                 devices=None, distributed=None):
+                 devices=None, distributed=None, nccl=None):
         self.mesh, self.order = mesh, order
         self.prec = 8 if precision in ("f64", 8) else 4
         self.dtype = np.float64 if self.prec == 8 else np.float32
         self.gas = gas or Gas(1.4, 287.0, 1e5, 9.81)
         self.settings = settings or Settings(1, 0, 0.0, 0.0, 0.0)
         h = C.c_void_p()
-        if distributed is None:
+        if nccl is not None:
+            # one process per GPU, the exchange in the library (ncclSend/ncclRecv):
+            # nccl = (world_size, rank, device, 128-byte unique id)
+            world, rank, device, uid = nccl
+            buf = (C.c_ubyte * 128).from_buffer_copy(bytes(uid))
+            check(lib().esdg_b200_solver_create_nccl(
+                mesh.h, order, C.byref(self.gas), C.byref(self.settings), self.prec, world, rank,
+                device, buf, C.byref(h)))
+        elif distributed is None:
             dev = np.ascontiguousarray(devices if devices is not None else [0], np.int32)
             check(lib().esdg_b200_solver_create(mesh.h, order, C.byref(self.gas), C.byref(self.settings),
                                                 self.prec, ranks, dev.ctypes.data_as(_ip), dev.size,
@@ -379,6 +395,7 @@ class GpuSolver:
                 mesh.h, order, C.byref(self.gas), C.byref(self.settings), self.prec, world, rank,
                 device, self._cb, None, C.byref(h)))
         self.h = h
+        self.rank0 = 0 if (distributed is None and nccl is None) else (distributed or nccl)[1]
         self.n3 = int(lib().esdg_b200_solver_n3(h))
         self.nq = order + 1
         self.begin = int(lib().esdg_b200_solver_local_begin(h))
@@ -395,6 +412,26 @@ class GpuSolver:
 
     def set_path(self, path):
         self._chk(lib().esdg_b200_solver_set_path(self.h, path))
+
+    def set_variant(self, variant):
+        """KernelVariant (kernels.hpp:27-34): 0 baseline .. 5 balanced."""
+        self._chk(lib().esdg_b200_solver_set_variant(self.h, variant))
+
+    def record_events(self, on=True):
+        self._chk(lib().esdg_b200_solver_record_events(self.h, 1 if on else 0))
+
+    def rank_events(self, rank=None):
+        """RankEvents of the last recorded RHS of partition `rank` (default: the
+        first local one), ns since that RHS was enqueued."""
+        ns = np.zeros(5, np.int64)
+        r = self.rank0 if rank is None else rank
+        self._chk(lib().esdg_b200_solver_rank_events(self.h, r, ns.ctypes.data_as(_i64p)))
+        return dict(zip(("sends_posted_ns", "volume_start_ns", "volume_end_ns", "wait_end_ns",
+                         "last_arrival_ns"), (int(x) for x in ns)))
+
+    @property
+    def halo_bytes(self) -> int:
+        return int(lib().esdg_b200_solver_halo_bytes(self.h))
 
     def set_overlap(self, on):
         self._chk(lib().esdg_b200_solver_set_overlap(self.h, 1 if on else 0))
@@ -535,6 +572,13 @@ class GpuSolver:
         n = lib().esdg_b200_solver_halo(self.h, peer.ctypes.data_as(_ip), off.ctypes.data_as(_i64p),
                                         cnt.ctypes.data_as(_i64p), cap)
         return [(int(peer[i]), int(off[i]), int(cnt[i])) for i in range(n)]
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it, the host distributes it)."""
+    buf = (C.c_ubyte * 128)()
+    check(lib().esdg_b200_nccl_unique_id(buf))
+    return bytes(buf)
 
 
 def selftest(device=0, precision=8):

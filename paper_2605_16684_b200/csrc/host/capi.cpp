@@ -2,6 +2,7 @@
 // the reference's mesh / partition / Solver interface behind C handles.
 #include <cstring>
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "esdg_b200.h"
@@ -209,6 +210,35 @@ int esdg_b200_solver_create_distributed(esdg_b200_mesh* mesh, int order,
   return make_solver(mesh, opt, out);
 }
 
+int esdg_b200_nccl_unique_id(void* id128) {
+  if (!id128) return ESDG_B200_BADARG;
+  std::string why;
+  if (!esdg_b200::host::NcclTransport::unique_id(id128, &why)) {
+    esdg_b200::set_message("nccl_unique_id: " + why);
+    return ESDG_B200_CUDA;
+  }
+  return ESDG_B200_OK;
+}
+
+int esdg_b200_solver_create_nccl(esdg_b200_mesh* mesh, int order, const esdg_b200_gas* gas,
+                                 const esdg_b200_settings* settings, int precision,
+                                 int world_size, int rank, int device, const void* id128,
+                                 esdg_b200_solver** out) {
+  if (!gas || !settings || !id128 || world_size < 1 || rank < 0 || rank >= world_size)
+    return ESDG_B200_BADARG;
+  SolverCore::Options opt;
+  opt.order = order;
+  opt.precision = precision;
+  opt.gas = *gas;
+  opt.settings = *settings;
+  opt.world_size = world_size;
+  opt.local_ranks = {rank};
+  opt.devices = {device};
+  opt.nccl = true;
+  std::memcpy(opt.nccl_id, id128, sizeof opt.nccl_id);
+  return make_solver(mesh, opt, out);
+}
+
 void esdg_b200_solver_destroy(esdg_b200_solver* s) {
   if (!s) return;
   delete s->core;
@@ -218,6 +248,16 @@ void esdg_b200_solver_destroy(esdg_b200_solver* s) {
 #define CORE(s) if (!(s)) return ESDG_B200_BADARG; SolverCore& c = *(s)->core
 
 int esdg_b200_solver_set_path(esdg_b200_solver* s, int path) { CORE(s); return c.set_path(path); }
+int esdg_b200_solver_set_variant(esdg_b200_solver* s, int variant) { CORE(s); return c.set_variant(variant); }
+int esdg_b200_solver_record_events(esdg_b200_solver* s, int on) { CORE(s); return c.record_events(on != 0); }
+int esdg_b200_solver_rank_events(esdg_b200_solver* s, int rank, int64_t ns[5]) {
+  CORE(s);
+  return c.rank_events(rank, ns);
+}
+int64_t esdg_b200_solver_halo_bytes(const esdg_b200_solver* s) {
+  return s ? s->core->halo_bytes_per_rhs() : 0;
+}
+int esdg_b200_solver_nccl_version(const esdg_b200_solver* s) { return s ? s->core->nccl_version() : 0; }
 int esdg_b200_solver_set_overlap(esdg_b200_solver* s, int on) {
   CORE(s);
   c.set_overlap(on != 0);

@@ -133,17 +133,29 @@ int SolverCore::create(Mesh* mesh, const Options& opt, SolverCore** out) {
     build_rank_halo(*mesh, s->range_begin_, lr[i], ls.halo);
     if (!ls.halo.peers.empty()) s->any_halo_ = true;
   }
-  // every peer must be local unless an exchange callback was given
-  if (!opt.exchange)
+  // every peer must be local unless an exchange callback or NCCL was given
+  if (!opt.exchange && !opt.nccl)
     for (const LocalShard& ls : s->shards_)
       for (const auto& p : ls.halo.peers)
         if (s->local_index_of_rank(p.rank) < 0) {
-          set_message("solver_create: remote peers need an exchange callback");
+          set_message("solver_create: remote peers need an exchange callback or NCCL");
           return ESDG_B200_BADARG;
         }
   for (size_t i = 0; i < s->shards_.size(); ++i) {
     const int rc = s->build_shard(s->shards_[i]);
     if (rc != ESDG_B200_OK) return rc;
+  }
+  if (opt.nccl) {
+    if (s->shards_.size() != 1) {
+      set_message("solver_create: NCCL exchange takes one partition per process");
+      return ESDG_B200_BADARG;
+    }
+    if (cudaSetDevice(opt.devices[0]) != cudaSuccess) return cuda_fail(cudaGetLastError(), "cudaSetDevice");
+    std::string why;
+    if (!s->nccl_.init(opt.world_size, lr.front(), opt.nccl_id, &why)) {
+      set_message("solver_create: " + why);
+      return ESDG_B200_CUDA;
+    }
   }
   // peer access between the devices of local shards (best effort)
   for (size_t i = 0; i < s->shards_.size(); ++i)
@@ -168,6 +180,8 @@ SolverCore::~SolverCore() {
     if (ls.ev_pack) cudaEventDestroy(ls.ev_pack);
     if (ls.ev_recv) cudaEventDestroy(ls.ev_recv);
     if (ls.ev_surf) cudaEventDestroy(ls.ev_surf);
+    for (cudaEvent_t e : ls.tl)
+      if (e) cudaEventDestroy(e);
   }
   for (auto& t : pending_) {
     cudaEventDestroy(t.a);
@@ -257,6 +271,15 @@ int SolverCore::build_shard(LocalShard& ls) {
   CU(cudaEventCreateWithFlags(&ls.ev_pack, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&ls.ev_recv, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&ls.ev_surf, cudaEventDisableTiming));
+  return ESDG_B200_OK;
+}
+
+int SolverCore::set_variant(int variant) {
+  if (variant < 0 || variant > 5) {
+    set_message("set_variant: KernelVariant is 0 (baseline) .. 5 (balanced)");
+    return ESDG_B200_BADARG;
+  }
+  variant_ = variant;
   return ESDG_B200_OK;
 }
 
@@ -490,18 +513,75 @@ int SolverCore::timers(double seconds[4], int64_t* launches, bool reset) {
 
 // ---- RHS -------------------------------------------------------------------
 
+// Timeline marks (RankEvents, exchange.hpp:83-89): timing-enabled events on
+// the partition's streams, recorded only while record_events() is on.
+enum { kTlStart = 0, kTlPosted, kTlKernelStart, kTlKernelEnd, kTlArrival, kTlWaitEnd };
+
+int SolverCore::mark(LocalShard& ls, int which, cudaStream_t st) {
+  if (!record_events_) return ESDG_B200_OK;
+  CU(cudaSetDevice(ls.dev->device()));
+  if (!ls.tl[which]) CU(cudaEventCreate(&ls.tl[which]));
+  CU(cudaEventRecord(ls.tl[which], st));
+  if (which == kTlStart) ls.tl_valid = true;
+  return ESDG_B200_OK;
+}
+
+int SolverCore::record_events(bool on) {
+  record_events_ = on;
+  return ESDG_B200_OK;
+}
+
+// ns since the RHS was enqueued: sends_posted, volume_start, volume_end,
+// wait_end, last_arrival (the member order of RankEvents). The overlap
+// property the reference tests with a delayed transport
+// (tests/test_partition.cpp:116-134) reads volume_start < last_arrival.
+int SolverCore::rank_events(int rank, int64_t ns[5]) {
+  const int idx = local_index_of_rank(rank);
+  if (idx < 0 || !ns) return ESDG_B200_BADARG;
+  LocalShard& ls = shards_[size_t(idx)];
+  for (int i = 0; i < 5; ++i) ns[i] = 0;
+  if (!ls.tl_valid) return ESDG_B200_OK;
+  CU(cudaSetDevice(ls.dev->device()));
+  CU(cudaStreamSynchronize(ls.dev->stream()));
+  if (ls.comm) CU(cudaStreamSynchronize(ls.comm));
+  const int order[5] = {kTlPosted, kTlKernelStart, kTlKernelEnd, kTlWaitEnd, kTlArrival};
+  for (int i = 0; i < 5; ++i) {
+    cudaEvent_t e = ls.tl[order[i]];
+    if (!e || cudaEventQuery(e) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ls.tl[kTlStart], e) != cudaSuccess) {
+      cudaGetLastError(); // an event of an earlier configuration (e.g. no halo)
+      continue;
+    }
+    ns[i] = int64_t(double(ms) * 1e6);
+  }
+  return ESDG_B200_OK;
+}
+
+int64_t SolverCore::halo_bytes_per_rhs() const {
+  int64_t bytes = 0;
+  for (const auto& ls : shards_)
+    bytes += int64_t(ls.halo.send_elem.size()) * int64_t(ls.dev->trace_bytes());
+  return bytes; // sent; the same amount is received
+}
+
 // (1) of rhs_job (solver.hpp:249-257): pack the ghost traces and start moving
 // them; returns immediately, copies run on the comm streams.
 int SolverCore::exchange_begin(int src) {
   for (auto& ls : shards_) {
+    RC(mark(ls, kTlStart, ls.dev->stream()));
     if (ls.halo.peers.empty()) continue;
     CU(cudaSetDevice(ls.dev->device()));
     // the previous RHS' copies out of this send buffer must have landed
-    if (!opt_.exchange)
+    if (!remote_peers())
       for (const auto& p : ls.halo.peers)
         CU(cudaStreamWaitEvent(ls.dev->stream(), shards_[size_t(local_index_of_rank(p.rank))].ev_recv, 0));
     RC(timed(ls, kClsPack, [&] { return ls.dev->pack(src, nullptr); }));
     CU(cudaEventRecord(ls.ev_pack, ls.dev->stream()));
+    RC(mark(ls, kTlPosted, ls.dev->stream()));
   }
   if (opt_.exchange) {
     LocalShard& ls = shards_[0];
@@ -509,6 +589,35 @@ int SolverCore::exchange_begin(int src) {
       set_message("exchange callback failed (phase 0)");
       return ESDG_B200_CUDA;
     }
+    return ESDG_B200_OK;
+  }
+  if (opt_.nccl) {
+    // one process per GPU: one ncclSend/ncclRecv pair per peer in one group on
+    // the copy stream, behind the pack kernel and behind the last reader of
+    // the receive buffer (the previous RHS' boundary kernel). The send buffer
+    // is safe to repack once ev_recv has fired: the group completes locally
+    // only after its sends have left.
+    LocalShard& ls = shards_[0];
+    if (ls.halo.peers.empty()) return ESDG_B200_OK;
+    CU(cudaSetDevice(ls.dev->device()));
+    CU(cudaStreamWaitEvent(ls.comm, ls.ev_pack, 0));
+    CU(cudaStreamWaitEvent(ls.comm, ls.ev_surf, 0));
+    const long long per = (long long)(5) * n2_;
+    std::vector<long long> off, cnt;
+    std::vector<int> peer;
+    for (const auto& p : ls.halo.peers) {
+      off.push_back((long long)(p.offset) * per);
+      cnt.push_back((long long)(p.count) * per);
+      peer.push_back(p.rank);
+    }
+    std::string why;
+    if (!nccl_.exchange(ls.dev->send_ptr(), ls.dev->recv_ptr(), off.data(), cnt.data(), peer.data(),
+                        int(peer.size()), opt_.precision, ls.comm, &why)) {
+      set_message("halo exchange: " + why);
+      return ESDG_B200_CUDA;
+    }
+    CU(cudaEventRecord(ls.ev_recv, ls.comm));
+    RC(mark(ls, kTlArrival, ls.comm));
     return ESDG_B200_OK;
   }
   for (auto& ls : shards_) {
@@ -530,6 +639,7 @@ int SolverCore::exchange_begin(int src) {
                              src_ls.dev->device(), size_t(p.count) * tb, ls.comm));
     }
     CU(cudaEventRecord(ls.ev_recv, ls.comm));
+    RC(mark(ls, kTlArrival, ls.comm));
   }
   return ESDG_B200_OK;
 }
@@ -541,12 +651,13 @@ int SolverCore::exchange_end() {
       set_message("exchange callback failed (phase 1)");
       return ESDG_B200_CUDA;
     }
-    return ESDG_B200_OK;
+    return mark(shards_[0], kTlWaitEnd, shards_[0].dev->stream());
   }
   for (auto& ls : shards_) {
     if (ls.halo.peers.empty()) continue;
     CU(cudaSetDevice(ls.dev->device()));
     CU(cudaStreamWaitEvent(ls.dev->stream(), ls.ev_recv, 0));
+    RC(mark(ls, kTlWaitEnd, ls.dev->stream()));
   }
   return ESDG_B200_OK;
 }
@@ -563,13 +674,17 @@ int SolverCore::rhs(int src, int dst, double a_old, double a_new,
     // wait-first order (set_overlap(0)): the one launch over all groups reads
     // the ghost traces, so the compute streams wait for them BEFORE it
     if (halo && !split) RC(exchange_end());
-    for (auto& ls : shards_)
+    for (auto& ls : shards_) {
+      if (!halo) RC(mark(ls, kTlStart, ls.dev->stream()));
+      RC(mark(ls, kTlKernelStart, ls.dev->stream()));
       RC(timed(ls, kClsVolume, [&] {
         return ls.dev->rhs(kModeFused, src, dst, a_old, a_new, source, stage,
                            split && !ls.halo.peers.empty() ? ESDG_B200_PART_INTERIOR
                                                            : ESDG_B200_PART_ALL,
                            nullptr);
       }));
+      RC(mark(ls, kTlKernelEnd, ls.dev->stream()));
+    }
     if (split) RC(exchange_end());
     for (auto& ls : shards_) {
       if (!halo || ls.halo.peers.empty()) continue;
@@ -584,10 +699,14 @@ int SolverCore::rhs(int src, int dst, double a_old, double a_new,
     return ESDG_B200_OK;
   }
   // (2) volume term overlaps the exchange (solver.hpp:259-262)
-  for (auto& ls : shards_)
+  for (auto& ls : shards_) {
+    if (!halo) RC(mark(ls, kTlStart, ls.dev->stream()));
+    RC(mark(ls, kTlKernelStart, ls.dev->stream()));
     RC(timed(ls, kClsVolume, [&] {
       return ls.dev->rhs(kModeVolume, src, dst, a_old, a_new, source, stage, ESDG_B200_PART_ALL, nullptr);
     }));
+    RC(mark(ls, kTlKernelEnd, ls.dev->stream()));
+  }
   if (volume_only) return ESDG_B200_OK;
   if (halo) RC(exchange_end());
   // (3)-(5) face fluxes and lift (solver.hpp:264-337)
@@ -612,13 +731,17 @@ int SolverCore::stage_fused(double a_old, double a_new, double b, int stage) {
   // wait-first order: see rhs()
   if (halo && !split) RC(exchange_end());
   // groups without a ghost face first: they hide the transfer
-  for (auto& ls : shards_)
+  for (auto& ls : shards_) {
+    if (!halo) RC(mark(ls, kTlStart, ls.dev->stream()));
+    RC(mark(ls, kTlKernelStart, ls.dev->stream()));
     RC(timed(ls, kClsVolume, [&] {
       return ls.dev->stage_fused(a_old, a_new, b, source, stage,
                                  split && !ls.halo.peers.empty() ? ESDG_B200_PART_INTERIOR
                                                                  : ESDG_B200_PART_ALL,
                                  nullptr);
     }));
+    RC(mark(ls, kTlKernelEnd, ls.dev->stream()));
+  }
   if (split) RC(exchange_end());
   for (auto& ls : shards_) {
     if (!halo || ls.halo.peers.empty()) continue;

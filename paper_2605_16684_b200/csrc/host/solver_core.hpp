@@ -17,6 +17,7 @@
 #include "esdg_b200.h"
 #include "host_types.hpp"
 #include "../shard_internal.hpp"
+#include "nccl_transport.hpp"
 
 namespace esdg_b200 {
 namespace host {
@@ -33,6 +34,10 @@ public:
     std::vector<int> devices;     // device of each local partition
     esdg_b200_exchange_fn exchange = nullptr; // set => peers are remote
     void* exchange_user = nullptr;
+    // set => peers are remote and reached by ncclSend/ncclRecv (one rank per
+    // process, communicator built from this unique id)
+    bool nccl = false;
+    unsigned char nccl_id[kNcclUniqueIdBytes] = {};
   };
 
   static int create(Mesh* mesh, const Options& opt, SolverCore** out);
@@ -48,6 +53,15 @@ public:
   const Mesh& mesh() const { return *mesh_; }
 
   int set_path(int path);
+  // KernelVariant (kernels.hpp:27-34): the ladder rung of the volume kernel
+  int set_variant(int variant);
+  int variant() const { return variant_; }
+  // RankEvents (exchange.hpp:83-89): CUDA-event timeline of the next RHS
+  // evaluations of every local partition
+  int record_events(bool on);
+  int rank_events(int rank, int64_t ns[5]);
+  int64_t halo_bytes_per_rhs() const;
+  int nccl_version() const { return nccl_.version(); }
   int step_swap(double dt, const void* host_in, void* host_out, bool do_check);
   void set_overlap(bool on) { overlap_ = on; }
   void overlap_elements(int64_t* interior, int64_t* total);
@@ -91,6 +105,11 @@ private:
     std::unique_ptr<ShardBase> dev;
     cudaStream_t comm = nullptr, down = nullptr; // copy streams (down: step_swap's D2H)
     cudaEvent_t ev_pack = nullptr, ev_recv = nullptr, ev_surf = nullptr;
+    // timeline of the last recorded RHS (timing enabled): start, traces
+    // packed and posted, first kernel start / end, last trace arrived,
+    // compute stream past its wait
+    cudaEvent_t tl[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    bool tl_valid = false;
   };
   struct TimedLaunch {
     cudaEvent_t a, b;
@@ -126,6 +145,11 @@ private:
   int path_ = ESDG_B200_PATH_STAGE; // the fastest; SPLIT keeps the reference's kernel structure
   int reduction_ = ESDG_B200_REDUCE_ON_DEVICE;
   bool any_halo_ = false;
+  bool remote_peers() const { return opt_.exchange != nullptr || opt_.nccl; }
+  int mark(LocalShard& ls, int which, cudaStream_t st);
+  NcclTransport nccl_;
+  int variant_ = 5; // balanced
+  bool record_events_ = false;
   bool overlap_ = true; // one-pass paths: interior groups hide the exchange
   esdg_b200_error err_{};
   bool timing_ = false;

@@ -69,3 +69,131 @@ def test_two_processes_equal_one(tmp_path, path):
     got_q = np.concatenate([np.load(tmp_path / f"q{r}.npy") for r in range(world)])
     assert np.array_equal(got_k, k)
     assert np.array_equal(got_q, g.get_state())
+
+
+# ---- the exchange in the library itself (NCCL bound in C++) --------------------
+
+def test_native_nccl_single_rank_and_event_timeline():
+    """esdg_b200_solver_create_nccl with world_size 1 (all a one-GPU box can
+    run): NCCL is bound at run time, the communicator comes up, the solver
+    steps, and the RankEvents timeline of a recorded RHS is ordered."""
+    uid = capi.nccl_unique_id()
+    assert len(uid) == 128 and any(uid)
+    mesh = capi.Mesh(capi.bubble_mesh_config(2, False))
+    s = capi.GpuSolver(mesh, 4, "f64", nccl=(1, 0, 0, uid))
+    assert capi.lib().esdg_b200_solver_nccl_version(s.h) >= 21800
+    s.init_case(capi.CASE_BUBBLE_SHARP)
+    ref = capi.GpuSolver(mesh, 4, "f64")
+    ref.init_case(capi.CASE_BUBBLE_SHARP)
+    dt = ref.compute_dt(0.5)
+    s.record_events(True)
+    for _ in range(3):
+        s.step(dt)
+        ref.step(dt)
+    assert np.array_equal(s.get_state(), ref.get_state())
+    ev = s.rank_events()
+    assert 0 <= ev["volume_start_ns"] < ev["volume_end_ns"]
+    assert s.halo_bytes == 0
+
+
+def test_event_timeline_shows_overlap_with_partitions():
+    """The GPU analogue of tests/test_partition.cpp:116-134 (a delayed
+    transport proves that volume work starts before the last trace arrives):
+    with four partitions on this device the kernel over the element groups
+    without a ghost face is enqueued right behind the pack kernel, while the
+    copies wait on every peer's pack. Recorded with CUDA events on the
+    partitions' streams: volume_start <= last_arrival on every partition that
+    has peers, wait_end >= last_arrival, and results stay bitwise."""
+    mesh = capi.Mesh(capi.bubble_mesh_config(3, False))
+    s = capi.GpuSolver(mesh, 4, "f64", ranks=4)
+    s.init_case(capi.CASE_BUBBLE_SHARP)
+    one = capi.GpuSolver(mesh, 4, "f64")
+    one.init_case(capi.CASE_BUBBLE_SHARP)
+    dt = one.compute_dt(0.5)
+    s.step(dt)                      # warm
+    one.step(dt)
+    s.record_events(True)
+    s.step(dt)
+    one.step(dt)
+    assert np.array_equal(s.get_state(), one.get_state())
+    assert s.halo_bytes > 0
+    overlapped = 0
+    for r in range(4):
+        ev = s.rank_events(r)
+        assert ev["sends_posted_ns"] > 0 and ev["last_arrival_ns"] > 0, ev
+        assert ev["wait_end_ns"] >= ev["last_arrival_ns"], ev
+        assert ev["volume_start_ns"] >= ev["sends_posted_ns"], ev
+        overlapped += ev["volume_start_ns"] <= ev["last_arrival_ns"]
+    assert overlapped >= 3
+
+
+def _n_devices():
+    return capi.lib().esdg_b200_device_count()
+
+
+@pytest.mark.parametrize("path", [capi.PATH_SPLIT, capi.PATH_STAGE])
+def test_partitions_on_several_devices_bitwise(path):
+    """In-process partitions on DIFFERENT GPUs (traces by cudaMemcpyPeerAsync
+    over NVLink): bitwise the one-device result. Needs >= 2 devices."""
+    n = _n_devices()
+    if n < 2:
+        pytest.skip("one GPU visible")
+    mesh = capi.Mesh(capi.bubble_mesh_config(3, False))
+    one = capi.GpuSolver(mesh, 4, "f64")
+    one.set_path(path)
+    one.init_case(capi.CASE_BUBBLE_SHARP)
+    dt = one.compute_dt(0.5)
+    for _ in range(5):
+        one.step(dt)
+    for parts in sorted({2, min(4, n), min(8, n)}):
+        s = capi.GpuSolver(mesh, 4, "f64", ranks=parts, devices=list(range(parts)))
+        s.set_path(path)
+        s.init_case(capi.CASE_BUBBLE_SHARP)
+        for _ in range(5):
+            s.step(dt)
+        assert np.array_equal(s.get_state(), one.get_state()), parts
+
+
+def _nccl_worker(rank, world, path, out_dir):
+    torch.cuda.set_device(rank)
+    id_file = os.path.join(out_dir, "nccl_id.bin")
+    if rank == 0:
+        with open(id_file + ".tmp", "wb") as f:
+            f.write(capi.nccl_unique_id())
+        os.replace(id_file + ".tmp", id_file)
+    else:
+        import time
+        while not os.path.exists(id_file):
+            time.sleep(0.01)
+    uid = open(id_file, "rb").read()
+    mesh = capi.Mesh(capi.bubble_mesh_config(3, False))
+    s = capi.GpuSolver(mesh, 4, "f64", nccl=(world, rank, rank, uid))
+    s.set_path(path)
+    s.init_case(capi.CASE_BUBBLE_SHARP)
+    dt = 0.0621602889129292      # compute_dt(0.5) of the whole mesh (BASELINE.md section 4)
+    s.record_events(True)
+    for _ in range(5):
+        s.step(dt)
+    np.save(os.path.join(out_dir, f"q{rank}.npy"), s.get_state())
+    np.save(os.path.join(out_dir, f"ev{rank}.npy"), np.array(list(s.rank_events().values())))
+    del s
+
+
+@pytest.mark.parametrize("path", [capi.PATH_SPLIT, capi.PATH_STAGE])
+def test_native_nccl_processes_bitwise(tmp_path, path):
+    """One process per GPU, traces by ncclSend/ncclRecv issued from C++ (no
+    Python inside step): the union of the ranks' states equals the one-process
+    state bitwise (tests/test_partition.cpp:94-114). Needs >= 2 devices."""
+    n = _n_devices()
+    if n < 2:
+        pytest.skip("one GPU visible")
+    world = min(n, 4)
+    mp.spawn(_nccl_worker, args=(world, path, str(tmp_path)), nprocs=world, join=True)
+    mesh = capi.Mesh(capi.bubble_mesh_config(3, False))
+    one = capi.GpuSolver(mesh, 4, "f64")
+    one.set_path(path)
+    one.init_case(capi.CASE_BUBBLE_SHARP)
+    for _ in range(5):
+        one.step(0.0621602889129292)
+    got = np.concatenate([np.load(tmp_path / f"q{r}.npy") for r in range(world)])
+    assert np.array_equal(got, one.get_state())
