@@ -458,6 +458,10 @@ def main_b200(args, rank, local_rank, world):
     peaks, peak_src = measured_peaks()
     fma_peak = capi.measure_fma_peak(device, rb)
     fma3_peak = capi.measure_fma_peak(device, rb, vector_operands=3)
+    # nominal CUDA-core FMA peak: SMs x FP64 (FP32) lanes x 2 x max SM clock
+    sm_count = torch.cuda.get_device_properties(device).multi_processor_count
+    sm_mhz = (clocks or {}).get("sm_max_mhz") or peaks.get("sm_max_mhz") or 1965.0
+    peak_nominal = sm_count * (64 if rb == 8 else 128) * 2 * sm_mhz * 1e6 / 1e12
     w = work_model(nq, rb)
     per_launch = {k: timers[k] / n_rhs for k in ("volume", "surface", "update")}
     kernels = {}
@@ -509,10 +513,6 @@ def main_b200(args, rank, local_rank, world):
                               "unit": "GB/s", "frac": surf_gbs / peaks["hbm_gbs"],
                               "ms": 1e3 * per_launch["surface"]}
     achieved = flops / dom_s / 1e12
-    # nominal CUDA-core FMA peak: SMs x FP64 (FP32) lanes x 2 x max SM clock
-    sm_count = torch.cuda.get_device_properties(device).multi_processor_count
-    sm_mhz = (clocks or {}).get("sm_max_mhz") or peaks.get("sm_max_mhz") or 1965.0
-    peak_nominal = sm_count * (64 if rb == 8 else 128) * 2 * sm_mhz * 1e6 / 1e12
     # the HBM side of the same kernel: its algorithmic bytes per element
     # over the same launch time
     stage_bytes = {"stage": 21 * nq ** 3 * rb, "fused": 16 * nq ** 3 * rb, "volume": w["volume_bytes"]}[traffic_key]

@@ -375,6 +375,12 @@ int esdg_b200_solver_set_variant(esdg_b200_solver* s, int variant);
  * transport reads volume_start < last_arrival. */
 int esdg_b200_solver_record_events(esdg_b200_solver* s, int on);
 int esdg_b200_solver_rank_events(esdg_b200_solver* s, int rank, int64_t ns[5]);
+/* Test hook, the analogue of Transport::send_hook (exchange.hpp:30): every
+ * partition's trace transfer is held back by `microseconds` on its copy
+ * stream (in-process copies and NCCL). Results must not change
+ * (tests/test_partition.cpp:136-152); with recording on, the timeline shows
+ * the kernels that do not need the traces running meanwhile. 0 = off. */
+int esdg_b200_solver_set_exchange_delay(esdg_b200_solver* s, int microseconds);
 /* bytes of face traces this process sends (and receives) per RHS */
 int64_t esdg_b200_solver_halo_bytes(const esdg_b200_solver* s);
 /* PATH_FUSED / PATH_STAGE with several partitions: on (default) runs the

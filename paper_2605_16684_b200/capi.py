@@ -128,6 +128,7 @@ SIGNATURES = {
     "esdg_b200_solver_record_events": (_i, [_vp, _i]),
     "esdg_b200_solver_rank_events": (_i, [_vp, _i, _i64p]),
     "esdg_b200_solver_halo_bytes": (_i64, [_vp]),
+    "esdg_b200_solver_set_exchange_delay": (_i, [_vp, _i]),
     "esdg_b200_solver_destroy": (None, [_vp]),
     "esdg_b200_solver_set_path": (_i, [_vp, _i]),
     "esdg_b200_solver_set_overlap": (_i, [_vp, _i]),
@@ -416,6 +417,10 @@ class GpuSolver:
     def set_variant(self, variant):
         """KernelVariant (kernels.hpp:27-34): 0 baseline .. 5 balanced."""
         self._chk(lib().esdg_b200_solver_set_variant(self.h, variant))
+
+    def set_exchange_delay(self, microseconds):
+        """Transport::send_hook analogue: hold every trace transfer back."""
+        self._chk(lib().esdg_b200_solver_set_exchange_delay(self.h, int(microseconds)))
 
     def record_events(self, on=True):
         self._chk(lib().esdg_b200_solver_record_events(self.h, 1 if on else 0))

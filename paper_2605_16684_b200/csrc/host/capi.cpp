@@ -254,6 +254,11 @@ int esdg_b200_solver_rank_events(esdg_b200_solver* s, int rank, int64_t ns[5]) {
   CORE(s);
   return c.rank_events(rank, ns);
 }
+int esdg_b200_solver_set_exchange_delay(esdg_b200_solver* s, int microseconds) {
+  CORE(s);
+  c.set_exchange_delay(microseconds);
+  return ESDG_B200_OK;
+}
 int64_t esdg_b200_solver_halo_bytes(const esdg_b200_solver* s) {
   return s ? s->core->halo_bytes_per_rhs() : 0;
 }

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -526,6 +527,20 @@ int SolverCore::mark(LocalShard& ls, int which, cudaStream_t st) {
   return ESDG_B200_OK;
 }
 
+namespace {
+void CUDART_CB sleep_on_stream(void* us) {
+  std::this_thread::sleep_for(std::chrono::microseconds(reinterpret_cast<intptr_t>(us)));
+}
+} // namespace
+
+// holds the copy stream back (host function; no CUDA call inside)
+int SolverCore::delay(LocalShard& ls) {
+  if (exchange_delay_us_ <= 0) return ESDG_B200_OK;
+  CU(cudaLaunchHostFunc(ls.comm, sleep_on_stream,
+                        reinterpret_cast<void*>(static_cast<intptr_t>(exchange_delay_us_))));
+  return ESDG_B200_OK;
+}
+
 int SolverCore::record_events(bool on) {
   record_events_ = on;
   return ESDG_B200_OK;
@@ -602,6 +617,7 @@ int SolverCore::exchange_begin(int src) {
     CU(cudaSetDevice(ls.dev->device()));
     CU(cudaStreamWaitEvent(ls.comm, ls.ev_pack, 0));
     CU(cudaStreamWaitEvent(ls.comm, ls.ev_surf, 0));
+    RC(delay(ls));
     const long long per = (long long)(5) * n2_;
     std::vector<long long> off, cnt;
     std::vector<int> peer;
@@ -616,8 +632,8 @@ int SolverCore::exchange_begin(int src) {
       set_message("halo exchange: " + why);
       return ESDG_B200_CUDA;
     }
+    RC(mark(ls, kTlArrival, ls.comm)); // before ev_recv: wait_end can only follow it
     CU(cudaEventRecord(ls.ev_recv, ls.comm));
-    RC(mark(ls, kTlArrival, ls.comm));
     return ESDG_B200_OK;
   }
   for (auto& ls : shards_) {
@@ -625,6 +641,7 @@ int SolverCore::exchange_begin(int src) {
     CU(cudaSetDevice(ls.dev->device()));
     // the receive buffer is free once the previous surface kernel has run
     CU(cudaStreamWaitEvent(ls.comm, ls.ev_surf, 0));
+    RC(delay(ls));
     const size_t tb = ls.dev->trace_bytes();
     for (const auto& p : ls.halo.peers) {
       LocalShard& src_ls = shards_[size_t(local_index_of_rank(p.rank))];
@@ -638,8 +655,8 @@ int SolverCore::exchange_begin(int src) {
                              static_cast<const char*>(src_ls.dev->send_ptr()) + size_t(peer_off) * tb,
                              src_ls.dev->device(), size_t(p.count) * tb, ls.comm));
     }
-    CU(cudaEventRecord(ls.ev_recv, ls.comm));
     RC(mark(ls, kTlArrival, ls.comm));
+    CU(cudaEventRecord(ls.ev_recv, ls.comm));
   }
   return ESDG_B200_OK;
 }

@@ -61,6 +61,9 @@ public:
   int record_events(bool on);
   int rank_events(int rank, int64_t ns[5]);
   int64_t halo_bytes_per_rhs() const;
+  // test hook, the analogue of Transport::send_hook (exchange.hpp:30): every
+  // partition's trace transfer is held back by `us` microseconds
+  void set_exchange_delay(int us) { exchange_delay_us_ = us < 0 ? 0 : us; }
   int nccl_version() const { return nccl_.version(); }
   int step_swap(double dt, const void* host_in, void* host_out, bool do_check);
   void set_overlap(bool on) { overlap_ = on; }
@@ -150,6 +153,8 @@ private:
   NcclTransport nccl_;
   int variant_ = 5; // balanced
   bool record_events_ = false;
+  int exchange_delay_us_ = 0;
+  int delay(LocalShard& ls);
   bool overlap_ = true; // one-pass paths: interior groups hide the exchange
   esdg_b200_error err_{};
   bool timing_ = false;

@@ -96,35 +96,42 @@ def test_native_nccl_single_rank_and_event_timeline():
     assert s.halo_bytes == 0
 
 
-def test_event_timeline_shows_overlap_with_partitions():
-    """The GPU analogue of tests/test_partition.cpp:116-134 (a delayed
-    transport proves that volume work starts before the last trace arrives):
-    with four partitions on this device the kernel over the element groups
-    without a ghost face is enqueued right behind the pack kernel, while the
-    copies wait on every peer's pack. Recorded with CUDA events on the
-    partitions' streams: volume_start <= last_arrival on every partition that
-    has peers, wait_end >= last_arrival, and results stay bitwise."""
+@pytest.mark.parametrize("path", [capi.PATH_SPLIT, capi.PATH_FUSED, capi.PATH_STAGE])
+def test_delayed_exchange_overlap_and_results(path):
+    """The GPU analogue of tests/test_partition.cpp:116-152: with the trace
+    transfer held back (esdg_b200_solver_set_exchange_delay, the counterpart
+    of Transport::send_hook) the kernel that needs no ghost trace -- the
+    volume kernel, or the one-pass kernel over the element groups without a
+    ghost face -- starts BEFORE the last trace arrives, the ghost-face work
+    waits for it, and the results are bitwise those of the undelayed run.
+    Recorded with CUDA events on the partitions' own streams."""
     mesh = capi.Mesh(capi.bubble_mesh_config(3, False))
     s = capi.GpuSolver(mesh, 4, "f64", ranks=4)
+    s.set_path(path)
     s.init_case(capi.CASE_BUBBLE_SHARP)
     one = capi.GpuSolver(mesh, 4, "f64")
+    one.set_path(path)
     one.init_case(capi.CASE_BUBBLE_SHARP)
     dt = one.compute_dt(0.5)
     s.step(dt)                      # warm
     one.step(dt)
+    s.set_exchange_delay(3000)      # 3 ms per RHS, a kernel takes ~50 us here
     s.record_events(True)
     s.step(dt)
     one.step(dt)
     assert np.array_equal(s.get_state(), one.get_state())
     assert s.halo_bytes > 0
-    overlapped = 0
     for r in range(4):
         ev = s.rank_events(r)
-        assert ev["sends_posted_ns"] > 0 and ev["last_arrival_ns"] > 0, ev
+        assert ev["sends_posted_ns"] > 0, ev
+        assert ev["last_arrival_ns"] >= 3_000_000, ev
+        assert ev["sends_posted_ns"] <= ev["volume_start_ns"] < ev["last_arrival_ns"], ev
+        assert ev["volume_end_ns"] < ev["last_arrival_ns"], ev      # the whole kernel hid behind the transfer
         assert ev["wait_end_ns"] >= ev["last_arrival_ns"], ev
-        assert ev["volume_start_ns"] >= ev["sends_posted_ns"], ev
-        overlapped += ev["volume_start_ns"] <= ev["last_arrival_ns"]
-    assert overlapped >= 3
+    s.set_exchange_delay(0)
+    s.step(dt)
+    one.step(dt)
+    assert np.array_equal(s.get_state(), one.get_state())
 
 
 def _n_devices():

