@@ -392,6 +392,13 @@ int64_t esdg_b200_solver_halo_bytes(const esdg_b200_solver* s);
 int esdg_b200_solver_set_overlap(esdg_b200_solver* s, int on);
 int esdg_b200_solver_overlap_elements(esdg_b200_solver* s, int64_t* interior,
                                       int64_t* total);
+/* PATH_FUSED / PATH_STAGE: on (default) evaluates every interior face once --
+ * by the element on its minus side, which hands the other element its share
+ * through device memory -- the way the reference keeps one record per face
+ * (compute_face_record, kernels.hpp:350-384; commit_face_side reads it for
+ * both sides). Off: every element evaluates all six of its faces. Results are
+ * bitwise the same either way and for every partition count. */
+int esdg_b200_solver_set_face_sharing(esdg_b200_solver* s, int on);
 int esdg_b200_solver_set_settings(esdg_b200_solver* s,
                                   const esdg_b200_settings* settings);
 int64_t esdg_b200_solver_local_begin(const esdg_b200_solver* s);

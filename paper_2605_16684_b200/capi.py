@@ -132,6 +132,7 @@ SIGNATURES = {
     "esdg_b200_solver_destroy": (None, [_vp]),
     "esdg_b200_solver_set_path": (_i, [_vp, _i]),
     "esdg_b200_solver_set_overlap": (_i, [_vp, _i]),
+    "esdg_b200_solver_set_face_sharing": (_i, [_vp, _i]),
     "esdg_b200_solver_overlap_elements": (_i, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "esdg_b200_solver_set_settings": (_i, [_vp, C.POINTER(Settings)]),
     "esdg_b200_solver_local_begin": (_i64, [_vp]),
@@ -440,6 +441,9 @@ class GpuSolver:
 
     def set_overlap(self, on):
         self._chk(lib().esdg_b200_solver_set_overlap(self.h, 1 if on else 0))
+
+    def set_face_sharing(self, on):
+        self._chk(lib().esdg_b200_solver_set_face_sharing(self.h, 1 if on else 0))
 
     def overlap_elements(self):
         """(elements whose work hides the halo exchange, all local elements)"""

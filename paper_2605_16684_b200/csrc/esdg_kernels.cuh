@@ -80,6 +80,18 @@ struct RhsParams {
   Real negd[NQ * NQ];    // -(2 D_ij); with metric[d]: -(2 g_d D_ij), kernels.hpp:187, 224-225
   Real metric[3];        // g_d = 2 / dx_d
   Real lift[3];          // Operators::face_coef, kernels.hpp:86-88
+  // One-pass kernels: every interior face is evaluated ONCE, by the element on
+  // its minus side (whose + face, lf odd, it is), which also works out the
+  // lift term of the plus side and pushes it into that element's slot of
+  // `frec`; the plus side picks it up when the sweep of that direction has
+  // its sums ready. face_roles[e]: bit f (0..2) = the lift term of face
+  // lf = 2f of e is pushed by the neighbour, bit 3+d = the term of face
+  // lf = 2d+1 is to be pushed to the neighbour. Null: every element evaluates
+  // all six faces. A slot holds an all-ones NaN until it has been filled and
+  // is set back to it by its reader (see rhs_kernel, "pulls").
+  const uint8_t* face_roles;
+  Real* frec;            // [element][3][5][FrecPitch<NQ>]: slot f = face lf = 2f
+  unsigned long long* sync_error;
   int flat_phi;          // phi is constant along x and y lines (checked by the host)
   int prefetch_ctas;     // resident CTAs chip-wide: L2 prefetch distance
   int with_source;       // Coriolis on (commit_volume, solver.hpp:205-216)
@@ -208,9 +220,15 @@ struct SmemMap {
   static constexpr size_t up16(size_t x) { return (x + 15) & ~size_t(15); }
   static constexpr size_t kStagePhi = up16(size_t(EPB) * 5 * G::N3 * sizeof(Real) + 16);
   static constexpr size_t kTend = up16(size_t(V_COUNT) * VS * sizeof(Real));
-  static constexpr size_t kTab = kTend + up16((size_t(5) * VS + 4) * sizeof(Real));
-  static constexpr size_t kBar = kTab + up16(size_t(LogTab<Real>::kReals) * sizeof(Real));
-  static constexpr size_t kBytes = kBar + 16;
+  // (slack words only where the slab takes `out` by bulk copy)
+  static constexpr size_t kTab = kTend + up16((size_t(5) * VS + (kBulk ? 4 : 0)) * sizeof(Real));
+  // The logarithm table with the mbarrier behind it; both are done with when
+  // the sweeps begin, and the landing area of the pulled lift terms
+  // (RhsParams::frec, [5][threads]) takes their place.
+  static constexpr size_t kTabBytes = up16(size_t(LogTab<Real>::kReals) * sizeof(Real));
+  static constexpr size_t kPull = size_t(5) * EPB * NQ * NQ * sizeof(Real);
+  static constexpr size_t kBar = kTab + kTabBytes;
+  static constexpr size_t kBytes = kTab + up16(kTabBytes + 16 > kPull ? kTabBytes + 16 : kPull);
   static_assert(kStagePhi + up16(size_t(EPB) * G::N3 * sizeof(Real) + 16) <= kTend,
                 "q and phi staging must fit in front of the slab");
 };
@@ -509,6 +527,37 @@ struct NbrRaw {
   int code;
 };
 
+// Raw state across one face node. code >= 0: local neighbour element, node
+// n_nb of it (the opposite side, same tangential position); code <= -2: ghost
+// trace slot, face node fn; -1: reflecting wall (mirror_state,
+// physics.hpp:309-313): the element's own trace (node n_own) with the normal
+// momentum negated, phi+ = phi-.
+template <class Real, int NQ>
+__device__ __forceinline__ void gather_trace(const RhsParams<Real, NQ>& P, int code, int dir,
+                                             long long eg, int n_nb, int n_own, int fn,
+                                             NbrRaw<Real>& r) {
+  constexpr int N2 = NQ * NQ, N3 = N2 * NQ;
+  if (code >= 0) {
+    const Real* qn = P.q + static_cast<long long>(code) * (5 * N3);
+#pragma unroll
+    for (int v = 0; v < 5; ++v) r.q[v] = qn[v * N3 + n_nb];
+    r.ph = P.phi[static_cast<long long>(code) * N3 + n_nb];
+  } else if (code <= -2) {
+    const long long g = (-2 - code) >> 1;
+#pragma unroll
+    for (int v = 0; v < 5; ++v) r.q[v] = P.ghost_q[(g * 5 + v) * N2 + fn];
+    r.ph = P.ghost_phi[g * N2 + fn];
+  } else {
+    const Real* qo = P.q + eg * (5 * N3);
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      const Real x = qo[v * N3 + n_own];
+      r.q[v] = (v == 1 + dir) ? -x : x;
+    }
+    r.ph = P.phi[eg * N3 + n_own];
+  }
+}
+
 // Surface contribution of one face node of one element side, rotated frame
 // of `dir`: c[v] = lift (F*_v - n F_v(q_own)), to be SUBTRACTED from the
 // tendency (compute_face_record + commit_face_side, kernels.hpp:350-430).
@@ -597,6 +646,76 @@ __device__ __forceinline__ void face_pair_contribution(const RhsParams<Real, NQ>
   }
 }
 
+// One-pass kernels: the lift flux of one face node for the evaluating side
+// (fl_own) and, BOTH, for the element across the face (fl_nb) -- bitwise what
+// that element obtains when it evaluates the face itself with the arguments
+// swapped (a ghost face in another partitioning): the symmetric flux is the
+// same number, gravity and dissipation are exactly negated (see
+// face_pair_contribution), and the expressions below are the same ones with
+// those signs. Rotated frame of the face direction; the caller applies
+// lift_d (the -n F(q_own) part cancels against the volume term, OWN = false).
+template <class Real, int NQ, bool BOTH>
+__device__ __forceinline__ void face_fluxes(const RhsParams<Real, NQ>& P, const Node<Real>& own,
+                                            const Node<Real>& nb, int side, Real (&fl_own)[5],
+                                            Real (&fl_nb)[5]) {
+  const PairFlux<Real> pf = pair_flux(own, nb, P.gas.cg);
+  Real dd[5] = {Real(0), Real(0), Real(0), Real(0), Real(0)};
+  if (P.dissipation) matrix_dissipation(own, nb, pf.rho_log, pf.inv_blog, P.gas, dd);
+  {
+    const Real n_own = side ? Real(1) : Real(-1);
+    const Real g_own = pf.tg * own.hib;
+    const Real phi_own = own.hphi + own.hphi;
+    fl_own[0] = n_own * pf.f[0] - Real(0.5) * dd[0];
+    fl_own[1] = n_own * pf.f[1] + n_own * g_own - Real(0.5) * dd[1];
+    fl_own[2] = n_own * pf.f[2] - Real(0.5) * dd[2];
+    fl_own[3] = n_own * pf.f[3] - Real(0.5) * dd[3];
+    fl_own[4] = n_own * pf.f[4] - Real(0.5) * fma_(phi_own, dd[0], dd[4]);
+  }
+  if (BOTH) {
+    Real dn[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) dn[v] = P.dissipation ? -dd[v] : Real(0);
+    const Real n_nb = side ? Real(-1) : Real(1);
+    const Real g_nb = (-pf.tg) * nb.hib;
+    const Real phi_nb = nb.hphi + nb.hphi;
+    fl_nb[0] = n_nb * pf.f[0] - Real(0.5) * dn[0];
+    fl_nb[1] = n_nb * pf.f[1] + n_nb * g_nb - Real(0.5) * dn[1];
+    fl_nb[2] = n_nb * pf.f[2] - Real(0.5) * dn[2];
+    fl_nb[3] = n_nb * pf.f[3] - Real(0.5) * dn[3];
+    fl_nb[4] = n_nb * pf.f[4] - Real(0.5) * fma_(phi_nb, dn[0], dn[4]);
+  }
+}
+
+// Rows of frec are padded to whole 128-byte lines: a line then belongs to one
+// (element, face, variable) and is read exactly once per launch, by the
+// element it is meant for, so no SM can hold a stale copy of it in L1.
+template <int NQ>
+struct FrecPitch {
+  static constexpr int value = (NQ * NQ + 15) & ~15;
+};
+// "Not filled yet": all ones, a NaN no arithmetic produces.
+__device__ __forceinline__ bool is_unfilled(double x) { return __double_as_longlong(x) == -1ll; }
+__device__ __forceinline__ bool is_unfilled(float x) { return __float_as_int(x) == -1; }
+__device__ __forceinline__ void set_unfilled(double* p) {
+  *reinterpret_cast<long long*>(p) = -1ll;
+}
+__device__ __forceinline__ void set_unfilled(float* p) { *reinterpret_cast<int*>(p) = -1; }
+// A lift term that has not arrived although the element evaluating it was
+// dispatched before this one: poll L2 until it is there. The element that
+// pushes never waits for anybody, so this ends; the loop is bounded all the
+// same and a time-out is reported to the host instead of hanging the device.
+template <class Real>
+__device__ __noinline__ Real wait_filled(const Real* src, unsigned long long* sync_error) {
+  Real x = __ldcg(src);
+#pragma unroll 1
+  for (int spins = 0; is_unfilled(x) && spins < (1 << 15); ++spins) {
+    __nanosleep(200);
+    x = __ldcg(src);
+  }
+  if (is_unfilled(x)) atomicOr(sync_error, 1ull);
+  return x;
+}
+
 template <class Real, int NQ, int EPB, int MINB, bool VOL, bool SURF>
 __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     rhs_kernel(const __grid_constant__ RhsParams<Real, NQ> P) {
@@ -611,6 +730,11 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   Real* vals = reinterpret_cast<Real*>(smem_raw);             // [V_COUNT][VS]
   Real* logtab = reinterpret_cast<Real*>(smem_raw + Map::kTab); // FP64 only: logarithm table
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(smem_raw + Map::kBar);
+  // one-pass kernels: landing area of the pulled lift terms, [5][threads]; it
+  // shares its place with the logarithm table, which is dead by then
+  Real* pbuf = logtab;
+  constexpr int FP = FrecPitch<NQ>::value;
+  constexpr int T = EPB * NQ * NQ;
 
   const int tid = threadIdx.x;
   const long long e0 =
@@ -650,10 +774,15 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   auto spitch = [](int ax) { return ax == 0 ? 1 : (ax == 1 ? PX : PX * NQ); };
   auto gpitch = [](int ax) { return ax == 0 ? 1 : (ax == 1 ? NQ : NQ * NQ); };
 
+  // the one-pass kernels keep the codes of the + faces only (the sweeps
+  // evaluate those); the - faces are looked at once, right before the commit
   int codes[6] = {-1, -1, -1, -1, -1, -1};
+  unsigned roles = 0;
   if (SURF && active) {
 #pragma unroll
-    for (int lf = 0; lf < 6; ++lf) codes[lf] = P.nbr[eg * 6 + lf];
+    for (int lf = 0; lf < 6; ++lf)
+      if (!VOL || (lf & 1)) codes[lf] = P.nbr[eg * 6 + lf];
+    if (VOL && P.face_roles) roles = P.face_roles[eg];
   }
 
   // Neighbour state of face lf, fetched one face ahead of its use so the
@@ -667,33 +796,11 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     const int d2 = d1 == 2 ? 0 : d1 + 1;
     r.code = lf == 0 ? codes[0] : lf == 1 ? codes[1] : lf == 2 ? codes[2]
              : lf == 3 ? codes[3] : lf == 4 ? codes[4] : codes[5];
-    if (r.code >= 0) {
-      // opposite side of the neighbour, same tangential (s, t)
-      const int n_nb = (side ? 0 : NQ - 1) * gpitch(dir) + l0 * gpitch(d1) +
-                       l1 * gpitch(d2);
-      const Real* qn = P.q + static_cast<long long>(r.code) * (5 * N3);
-#pragma unroll
-      for (int v = 0; v < 5; ++v) r.q[v] = qn[v * N3 + n_nb];
-      r.ph = P.phi[static_cast<long long>(r.code) * N3 + n_nb];
-    } else if (r.code <= -2) {
-      const long long g = (-2 - r.code) >> 1;
-#pragma unroll
-      for (int v = 0; v < 5; ++v) r.q[v] = P.ghost_q[(g * 5 + v) * N2 + l];
-      r.ph = P.ghost_phi[g * N2 + l];
-    } else {
-      // reflecting wall (mirror_state, physics.hpp:309-313): the element's own
-      // trace with the normal momentum negated, phi+ = phi-
-      const int n_own = (side ? NQ - 1 : 0) * gpitch(dir) + l0 * gpitch(d1) + l1 * gpitch(d2);
-      const Real* qo = P.q + eg * (5 * N3);
-#pragma unroll
-      for (int v = 0; v < 5; ++v) {
-        const Real x = qo[v * N3 + n_own];
-        r.q[v] = (v == 1 + dir) ? -x : x;
-      }
-      r.ph = P.phi[eg * N3 + n_own];
-    }
+    // thread (l0, l1) is face node (s, t) = (l0, l1): FaceIndexer::node
+    const int tang = l0 * gpitch(d1) + l1 * gpitch(d2);
+    gather_trace<Real, NQ>(P, r.code, dir, eg, (side ? 0 : NQ - 1) * gpitch(dir) + tang,
+                           (side ? NQ - 1 : 0) * gpitch(dir) + tang, l, r);
   };
-
   // ---- phase A: primitives and logarithms, once per node ------------------
   // All global loads are issued before the first logarithm, so the CTA pays
   // for one HBM round trip. In the accumulate form the old contents of `out`
@@ -790,6 +897,8 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   }
   ESDG_CLK();
   __syncthreads();
+  // the mbarrier's memory is reused as data later (SmemMap::kPull)
+  if (tid == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(mbar)) : "memory");
   ESDG_CLK();
   if (active) {
     if (SURF && !VOL) { // surface-only kernel: registers to spare, fetch early
@@ -809,11 +918,10 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     }
     const int bad = badmask ? __ffs(badmask) - 1 : -1;
     if (SURF && VOL) {
-      // the first direction's neighbour traces: issued here, not before the
-      // logarithms (26 registers the fused kernel's node loop cannot spare);
-      // they land while the CTA gathers at the barrier
-      fetch(0, cur[0]);
-      if (FPI == 2) fetch(1, cur[FPI - 1]);
+      // the trace across the first face the sweeps will evaluate: issued
+      // here, not before the logarithms (registers the fused kernel's node
+      // loop cannot spare); it lands while the CTA gathers at the barrier
+      fetch(1, cur[0]);
     }
     if (bad >= 0) {
       const Real* qb = qe + bad * N2;
@@ -827,14 +935,97 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   }
   ESDG_CLK();
   cp_async_wait_all(); // this thread's share of out_old is in the slab
-  __syncthreads();
+  if (VOL && SURF) {
+    // One-pass kernels: - faces (lf even) that no other element evaluates for
+    // this one -- walls, ghost faces, neighbours that come later in the launch
+    // order. Thread (l0, l1) is face node (s, t) = (l0, l1); the lift term
+    // goes to this element's own slot of frec, from where the z-line owners
+    // pick it up before the commit exactly like a pushed one. Only groups on
+    // the rim of a partition or of the mesh come through here.
+    if (__syncthreads_or(active && (roles & 7u) != 7u)) {
+      if (active) {
+#pragma unroll 1
+        for (int f = 0; f < 3; ++f) {
+          if (roles & (1u << f)) continue;
+          const int dir = f;
+          const int d1 = dir == 2 ? 0 : dir + 1;
+          const int d2 = d1 == 2 ? 0 : d1 + 1;
+          const int tang = l0 * gpitch(d1) + l1 * gpitch(d2);
+          NbrRaw<Real> raw[1];
+          raw[0].code = P.nbr[eg * 6 + 2 * f];
+          gather_trace<Real, NQ>(P, raw[0].code, dir, eg, (NQ - 1) * gpitch(dir) + tang, tang, l,
+                                 raw[0]);
+          Node<Real> nb[1];
+          face_pair_neighbours<Real, NQ, 1>(P, raw, dir, eg, l, logtab, nb);
+          const Node<Real> own =
+              load_node(vals, VS, e * N3P + l0 * spitch(d1) + l1 * spitch(d2), dir);
+          Real fl[5], unused[5];
+          face_fluxes<Real, NQ, false>(P, own, nb[0], 0, fl, unused);
+          const Real lift = P.lift[dir];
+          Real* rec = P.frec + ((eg * 3 + f) * 5) * FP + l;
+#pragma unroll
+          for (int v = 0; v < 5; ++v) rec[v * FP] = lift * fl[v];
+        }
+      }
+      // these slots are read through cp.async by other threads of the group
+      __syncthreads();
+    }
+  } else {
+    __syncthreads();
+  }
   ESDG_CLK();
 
   // ---- phase C: the six faces, thread per face node -----------------------
   // Every face subtracts its lift term from the shared tendency slab (zeroed
   // by the z-line owners in phase A). Faces of one direction share no node,
   // faces of different directions do (edges), hence the two barriers.
-  if (SURF) {
+  if (SURF && VOL) {
+    // One-pass kernels: only the three + faces (lf = 1, 3, 5) are evaluated
+    // here, for both elements they separate: this element's lift term goes to
+    // the slab, the other element's -- bitwise what it would compute itself,
+    // see face_fluxes -- to its slot of frec if it expects it (roles). Once
+    // every push of the group is out its flag goes up; that is long before
+    // any group dispatched later gets to its commit, where it needs them.
+#pragma unroll 1
+    for (int dir = 0; dir < 3; ++dir) {
+      if (active) {
+        const int d1 = dir == 2 ? 0 : dir + 1;
+        const int d2 = d1 == 2 ? 0 : d1 + 1;
+        Node<Real> nb[1];
+        const NbrRaw<Real>(&raw)[1] = reinterpret_cast<const NbrRaw<Real>(&)[1]>(cur[0]);
+        face_pair_neighbours<Real, NQ, 1>(P, raw, dir, eg, l, logtab, nb);
+        const int code = cur[0].code;
+        if (dir < 2) fetch(2 * dir + 3, cur[0]);
+        const int s_own = e * N3P + l0 * spitch(d1) + l1 * spitch(d2) + (NQ - 1) * spitch(dir);
+        const Node<Real> own = load_node(vals, VS, s_own, dir);
+        Real flo[5], fln[5];
+        face_fluxes<Real, NQ, true>(P, own, nb[0], 1, flo, fln);
+        const Real lift = P.lift[dir];
+        if (roles & (8u << dir)) {
+          Real* rec = P.frec + ((static_cast<long long>(code) * 3 + dir) * 5) * FP + l;
+#pragma unroll
+          for (int v = 0; v < 5; ++v) rec[v * FP] = lift * fln[v];
+        }
+        Real* tn = tslab + (1 + dir) * TV;
+        Real* tt1 = tslab + (1 + d1) * TV;
+        Real* tt2 = tslab + (1 + d2) * TV;
+        Real* t4 = tslab + 4 * TV;
+        Real o[5];
+        o[0] = tslab[s_own];
+        o[1] = tn[s_own];
+        o[2] = tt1[s_own];
+        o[3] = tt2[s_own];
+        o[4] = t4[s_own];
+        tslab[s_own] = fma_(-P.gain, lift * flo[0], o[0]);
+        tn[s_own] = fma_(-P.gain, lift * flo[1], o[1]);
+        tt1[s_own] = fma_(-P.gain, lift * flo[2], o[2]);
+        tt2[s_own] = fma_(-P.gain, lift * flo[3], o[3]);
+        t4[s_own] = fma_(-P.gain, lift * flo[4], o[4]);
+      }
+      __syncthreads();
+    }
+  }
+  if (SURF && !VOL) {
     // FPI faces per iteration (Tile<>::FPI). 2 = both faces of a direction as
     // two interleaved instruction streams: more ILP, but twice the loop
     // body. Where three or more CTAs in different phases share an SM the
@@ -899,6 +1090,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // x and y results are handed to the z-line owners through the shared slab;
   // the z sweep stays in registers because the same thread commits that line.
   Real acc[NQ][5];
+  Real pull_z[5] = {Real(0), Real(0), Real(0), Real(0), Real(0)}; // lift term of the - z face
 #pragma unroll
   for (int i = 0; i < NQ; ++i)
 #pragma unroll
@@ -918,12 +1110,54 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         for (int i = 0; i < NQ; ++i)
 #pragma unroll
           for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
+        // One-pass kernels, "pulls": the lift term of the - face this line
+        // starts on (lf = 2 dir) lies in the element's slot of frec -- pushed
+        // by the element across the face during its phase C, or put there by
+        // this group after phase A. The thread that sweeps a line is the face
+        // node (s, t) of the line's two faces: (l0, l1), for y lines (l1, l0).
+        // Asynchronous copies fetch the five values into shared memory while
+        // the pair fluxes are evaluated: no register is held for them and
+        // nobody waits for L2.
+        Real* slot = nullptr;
+        if (SURF) {
+          slot = P.frec + ((eg * 3 + dir) * 5) * FP + (dir == 1 ? l1 + NQ * l0 : l);
+#pragma unroll
+          for (int v = 0; v < 5; ++v) cp_async<sizeof(Real)>(&pbuf[v * T + tid], slot + v * FP);
+        }
         // x and y lines of a Cartesian mesh see a constant potential: no
         // gravity term there (a second, shorter code instance of the sweep)
         if (FlatXY<NQ, sizeof(Real)>::value && SURF && P.flat_phi && dir < 2)
           sweep_line<Real, NQ, !(VOL && SURF), true>(P, vals, VS, base, stride, dir, acc);
         else
           sweep_line<Real, NQ, !(VOL && SURF), false>(P, vals, VS, base, stride, dir, acc);
+        Real pull[5];
+        if (SURF) {
+          cp_async_wait_all();
+          bool filled = true;
+#pragma unroll
+          for (int v = 0; v < 5; ++v) {
+            pull[v] = pbuf[v * T + tid];
+            filled = filled && !is_unfilled(pull[v]);
+          }
+          if (!filled) {
+#pragma unroll 1
+            for (int v = 0; v < 5; ++v) {
+              const Real x = wait_filled(slot + v * FP, P.sync_error);
+              pull[0] = v == 0 ? x : pull[0];
+              pull[1] = v == 1 ? x : pull[1];
+              pull[2] = v == 2 ? x : pull[2];
+              pull[3] = v == 3 ? x : pull[3];
+              pull[4] = v == 4 ? x : pull[4];
+            }
+          }
+          // the slot is empty again for the next evaluation
+#pragma unroll
+          for (int v = 0; v < 5; ++v) set_unfilled(slot + v * FP);
+          if (dir == 2) {
+#pragma unroll
+            for (int v = 0; v < 5; ++v) pull_z[v] = pull[v];
+          }
+        }
         if (dir < 2) {
           // un-rotate into the slab: normal -> 1+dir, then cyclic. Without
           // faces the x sweep is the slab's first writer and simply stores;
@@ -951,6 +1185,11 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
             for (int i = 0; i < NQ; ++i)
 #pragma unroll
               for (int v = 0; v < 5; ++v) acc[i][v] = fma_(scale, acc[i][v], old[i][v]);
+            if (SURF) {
+              // the - face at the line's first node, same rotated frame
+#pragma unroll
+              for (int v = 0; v < 5; ++v) acc[0][v] = fma_(-P.gain, pull[v], acc[0][v]);
+            }
           } else {
 #pragma unroll
             for (int i = 0; i < NQ; ++i)
@@ -1025,6 +1264,14 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         knew[k][2] = fma_(zscale, acc[k][3], knew[k][2]);
         knew[k][3] = fma_(zscale, acc[k][1], knew[k][3]);
         knew[k][4] = fma_(zscale, acc[k][4], knew[k][4]);
+      }
+      if (SURF) {
+        // the - z face at the line's first node (normal -> var 3, x, y)
+        knew[0][0] = fma_(-P.gain, pull_z[0], knew[0][0]);
+        knew[0][3] = fma_(-P.gain, pull_z[1], knew[0][3]);
+        knew[0][1] = fma_(-P.gain, pull_z[2], knew[0][1]);
+        knew[0][2] = fma_(-P.gain, pull_z[3], knew[0][2]);
+        knew[0][4] = fma_(-P.gain, pull_z[4], knew[0][4]);
       }
       if (source) {
         // h = (0, f q2, -f q1, 0, 0)

@@ -268,6 +268,11 @@ int esdg_b200_solver_set_overlap(esdg_b200_solver* s, int on) {
   c.set_overlap(on != 0);
   return ESDG_B200_OK;
 }
+int esdg_b200_solver_set_face_sharing(esdg_b200_solver* s, int on) {
+  CORE(s);
+  c.set_face_sharing(on != 0);
+  return ESDG_B200_OK;
+}
 int esdg_b200_solver_overlap_elements(esdg_b200_solver* s, int64_t* interior, int64_t* total) {
   CORE(s);
   c.overlap_elements(interior, total);

@@ -67,6 +67,9 @@ public:
   int nccl_version() const { return nccl_.version(); }
   int step_swap(double dt, const void* host_in, void* host_out, bool do_check);
   void set_overlap(bool on) { overlap_ = on; }
+  void set_face_sharing(bool on) {
+    for (auto& ls : shards_) ls.dev->set_face_sharing(on ? 1 : 0);
+  }
   void overlap_elements(int64_t* interior, int64_t* total);
   int set_settings(const esdg_b200_settings& s);
   int halo(int32_t* peer, int64_t* offset, int64_t* count, int capacity) const;

@@ -245,9 +245,11 @@ public:
       CU(alloc_copy(&cor_f_, d.coriolis_f,
                     sizeof(Real) * size_t(d.n_ylevels) * size_t(nq_)));
     }
-    CU(cudaMalloc(&flag_, sizeof(unsigned long long)));
+    // [0] non-physical-state key, [1] a face-contribution wait timed out
+    CU(cudaMalloc(&flag_, 2 * sizeof(unsigned long long)));
+    CU(cudaMemset(flag_, 0, 2 * sizeof(unsigned long long)));
     CU(cudaMemcpy(flag_, &kNoFlag, sizeof kNoFlag, cudaMemcpyHostToDevice));
-    CU(cudaMallocHost(&flag_host_, sizeof(unsigned long long)));
+    CU(cudaMallocHost(&flag_host_, 2 * sizeof(unsigned long long)));
     CU(cudaMalloc(&flag_records_, sizeof(dev::FlagRecord) * dev::kFlagSlots));
     CU(cudaMemset(flag_records_, 0xff, sizeof(dev::FlagRecord) * dev::kFlagSlots));
     return ESDG_B200_OK;
@@ -298,6 +300,7 @@ public:
   size_t trace_bytes() const override { return sizeof(Real) * 5 * size_t(n2_); }
   int64_t launch_count() const override { return launches_; }
   void set_dissipation(int on) override { dissipation_ = on; }
+  void set_face_sharing(int on) override { share_faces_ = on; }
 
   int pack(int src, cudaStream_t st) override {
     if (src != 0 && src != 1) return bad("pack: bad register");
@@ -354,6 +357,11 @@ public:
       CU(cudaMalloc(&q_alt_, state_bytes + 64));
     }
     int rc = ESDG_B200_OK;
+    // the runs of one stage must come in ascending order, starting at group 0
+    // (an element pulls face contributions from elements before it)
+    if (first_group == 0) range_next_ = 0;
+    if (first_group != range_next_) return bad("stage_fused_range: runs must be consecutive from group 0");
+    range_next_ = first_group + n_groups;
     if (n_groups > 0) {
       range_first_ = first_group;
       range_count_ = n_groups;
@@ -456,11 +464,18 @@ public:
   int check(cudaStream_t st, int src, esdg_b200_error* err) override {
     CU(cudaSetDevice(device_));
     cudaStream_t s = pick(st);
-    CU(cudaMemcpyAsync(flag_host_, flag_, sizeof(unsigned long long),
+    CU(cudaMemcpyAsync(flag_host_, flag_, 2 * sizeof(unsigned long long),
                        cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
-    const unsigned long long key = *flag_host_;
+    const unsigned long long key = flag_host_[0];
     if (err) std::memset(err, 0, sizeof *err);
+    if (flag_host_[1] != 0) {
+      CU(cudaMemsetAsync(flag_ + 1, 0, sizeof(unsigned long long), s));
+      CU(cudaStreamSynchronize(s));
+      set_message("rhs_kernel: an element group waited in vain for the face contributions of an "
+                  "earlier group (launch order violated?)");
+      return ESDG_B200_CUDA;
+    }
     if (key == kNoFlag) return ESDG_B200_OK;
     CU(cudaMemcpyAsync(flag_, &kNoFlag, sizeof kNoFlag, cudaMemcpyHostToDevice, s));
     CU(cudaStreamSynchronize(s));
@@ -555,6 +570,13 @@ private:
     P.dissipation = dissipation_;
     P.flat_phi = flat_phi_;
     P.stage = stage;
+    // faces evaluated once and shared between the two elements (one-pass
+    // kernels only): the role table fits the order the groups of this launch
+    // are dispatched in
+    const bool share = mode == kModeFused && share_faces_ && frec_ != nullptr;
+    P.face_roles = share ? (groups ? roles_split_ : roles_all_) : nullptr;
+    P.frec = frec_;
+    P.sync_error = flag_ + 1;
     return launch_rhs<Real, NQ>(mode, P, n_groups, st);
   }
 
@@ -587,6 +609,37 @@ private:
     }
     n_groups_[0] = int64_t(interior.size());
     n_groups_[1] = int64_t(boundary.size());
+    // Face roles (RhsParams::face_roles). The face between A (its + face,
+    // lf odd) and B (its - face, lf - 1) is always evaluated by A. B takes
+    // A's result instead of evaluating the face a second time when A's group
+    // is dispatched no later than B's in the same launch: ascending group
+    // index for a launch over all groups (or over consecutive runs of them),
+    // and additionally the same list for the interior / boundary launches.
+    // Everything else -- walls, ghost faces, periodic wrap-around (A has the
+    // higher index there), faces between the two lists -- B evaluates itself.
+    std::vector<uint8_t> in_boundary(size_t(ng), 0);
+    for (int32_t g : boundary) in_boundary[size_t(g)] = 1;
+    std::vector<uint8_t> roles[2];
+    for (int t = 0; t < 2; ++t) {
+      std::vector<uint8_t>& r = roles[t];
+      r.assign(size_t(ne_), 0);
+      for (int64_t b = 0; b < ne_; ++b)
+        for (int f = 0; f < 3; ++f) {
+          const int32_t a = nbr[b * 6 + 2 * f];
+          if (a < 0 || a >= b || nbr[int64_t(a) * 6 + 2 * f + 1] != int32_t(b)) continue;
+          if (t == 1 && in_boundary[size_t(a / epb)] != in_boundary[size_t(b / epb)]) continue;
+          r[size_t(b)] |= uint8_t(1u << f);
+          r[size_t(a)] |= uint8_t(8u << f);
+        }
+    }
+    CU(alloc_copy(&roles_all_, roles[0].data(), size_t(ne_)));
+    CU(alloc_copy(&roles_split_, roles[1].data(), size_t(ne_)));
+    // slots of the pushed lift terms, all "not filled" (an all-ones NaN): rows
+    // padded to whole 128-byte lines (dev::FrecPitch)
+    const size_t frec_bytes =
+        sizeof(Real) * size_t(std::max<int64_t>(ne_, 1)) * 15 * size_t((n2_ + 15) & ~15);
+    CU(cudaMalloc(&frec_, frec_bytes));
+    CU(cudaMemset(frec_, 0xff, frec_bytes));
     interior.insert(interior.end(), boundary.begin(), boundary.end());
     CU(alloc_copy(&groups_, interior.data(), sizeof(int32_t) * interior.size()));
     return ESDG_B200_OK;
@@ -624,6 +677,9 @@ private:
     cudaFree(phi_);
     cudaFree(nbr_);
     cudaFree(groups_);
+    cudaFree(roles_all_);
+    cudaFree(roles_split_);
+    cudaFree(frec_);
     cudaFree(ghost_phi_);
     cudaFree(send_elem_);
     cudaFree(send_face_);
@@ -653,6 +709,11 @@ private:
           *ylevel_ = nullptr, *groups_ = nullptr;
   int64_t n_groups_[2] = {0, 0}, n_part_elems_[2] = {0, 0};
   int64_t range_first_ = 0, range_count_ = 0; // stage_fused_range: groups of this launch
+  int64_t range_next_ = 0;
+  // shared face evaluation of the one-pass kernels (RhsParams::face_roles)
+  uint8_t *roles_all_ = nullptr, *roles_split_ = nullptr;
+  Real* frec_ = nullptr;
+  int share_faces_ = 1;
   int epb_ = 1;
   unsigned long long *flag_ = nullptr, *flag_host_ = nullptr;
   double *red_out_ = nullptr, *red_tab_ = nullptr;

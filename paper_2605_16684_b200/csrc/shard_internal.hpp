@@ -29,6 +29,7 @@ public:
   virtual size_t trace_bytes() const = 0;
   virtual int64_t launch_count() const = 0;
   virtual void set_dissipation(int on) = 0;
+  virtual void set_face_sharing(int on) = 0;
   virtual int pack(int src, cudaStream_t st) = 0;
   // mode: RhsMode (esdg_launch.hpp); part: ESDG_B200_PART_* -- all elements,
   // or only the element groups without / with a ghost face
