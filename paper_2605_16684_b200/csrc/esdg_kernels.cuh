@@ -90,7 +90,7 @@ struct RhsParams {
   // all six faces. A slot holds an all-ones NaN until it has been filled and
   // is set back to it by its reader (see rhs_kernel, "pulls").
   const uint8_t* face_roles;
-  Real* frec;            // [element][3][5][FrecPitch<NQ>]: slot f = face lf = 2f
+  Real* frec;            // [3][element][FrecBlock<Real, NQ>]: slot f = face lf = 2f, [5][NQ^2] + pad
   unsigned long long* sync_error;
   int flat_phi;          // phi is constant along x and y lines (checked by the host)
   int prefetch_ctas;     // resident CTAs chip-wide: L2 prefetch distance
@@ -222,13 +222,20 @@ struct SmemMap {
   static constexpr size_t kTend = up16(size_t(V_COUNT) * VS * sizeof(Real));
   // (slack words only where the slab takes `out` by bulk copy)
   static constexpr size_t kTab = kTend + up16((size_t(5) * VS + (kBulk ? 4 : 0)) * sizeof(Real));
-  // The logarithm table with the mbarrier behind it; both are done with when
-  // the sweeps begin, and the landing area of the pulled lift terms
-  // (RhsParams::frec, [5][threads]) takes their place.
+  // The logarithm table is done with when the sweeps begin; the landing area
+  // of the pulled lift terms (RhsParams::frec: the group's blocks of one
+  // direction, one bulk copy) takes its place. The mbarrier outlives both.
+  // In the one configuration where 16 bytes decide the third resident CTA
+  // (padded FP64 layout, NQ = 4) the mbarrier sits in a padding slot of the
+  // last node-value array, which no copy and no thread touches.
   static constexpr size_t kTabBytes = up16(size_t(LogTab<Real>::kReals) * sizeof(Real));
-  static constexpr size_t kPull = size_t(5) * EPB * NQ * NQ * sizeof(Real);
-  static constexpr size_t kBar = kTab + kTabBytes;
-  static constexpr size_t kBytes = kTab + up16(kTabBytes + 16 > kPull ? kTabBytes + 16 : kPull);
+  static constexpr size_t kPullBlock = up16(size_t(5) * NQ * NQ * sizeof(Real)); // = FrecBlock bytes
+  static constexpr size_t kPull = size_t(EPB) * kPullBlock;
+  static constexpr size_t kRegion = kTabBytes > kPull ? kTabBytes : kPull;
+  static constexpr bool kBarInPad = !kBulk && sizeof(Real) == 8;
+  static constexpr size_t kBar =
+      kBarInPad ? (size_t(V_COUNT - 1) * VS + NQ) * sizeof(Real) : kTab + up16(kRegion);
+  static constexpr size_t kBytes = kTab + up16(kRegion) + (kBarInPad ? 0 : 16);
   static_assert(kStagePhi + up16(size_t(EPB) * G::N3 * sizeof(Real) + 16) <= kTend,
                 "q and phi staging must fit in front of the slab");
 };
@@ -686,12 +693,12 @@ __device__ __forceinline__ void face_fluxes(const RhsParams<Real, NQ>& P, const 
   }
 }
 
-// Rows of frec are padded to whole 128-byte lines: a line then belongs to one
-// (element, face, variable) and is read exactly once per launch, by the
-// element it is meant for, so no SM can hold a stale copy of it in L1.
-template <int NQ>
-struct FrecPitch {
-  static constexpr int value = (NQ * NQ + 15) & ~15;
+// One (direction, element) block of frec: [5][NQ^2] Reals, padded to a
+// multiple of 16 bytes so that the blocks of a group's consecutive elements
+// are one bulk copy.
+template <class Real, int NQ>
+struct FrecBlock {
+  static constexpr int value = int(((5 * NQ * NQ * sizeof(Real) + 15) & ~size_t(15)) / sizeof(Real));
 };
 // "Not filled yet": all ones, a NaN no arithmetic produces.
 __device__ __forceinline__ bool is_unfilled(double x) { return __double_as_longlong(x) == -1ll; }
@@ -733,8 +740,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // one-pass kernels: landing area of the pulled lift terms, [5][threads]; it
   // shares its place with the logarithm table, which is dead by then
   Real* pbuf = logtab;
-  constexpr int FP = FrecPitch<NQ>::value;
-  constexpr int T = EPB * NQ * NQ;
+  constexpr int FB = FrecBlock<Real, NQ>::value;
 
   const int tid = threadIdx.x;
   const long long e0 =
@@ -897,8 +903,6 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   }
   ESDG_CLK();
   __syncthreads();
-  // the mbarrier's memory is reused as data later (SmemMap::kPull)
-  if (tid == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(mbar)) : "memory");
   ESDG_CLK();
   if (active) {
     if (SURF && !VOL) { // surface-only kernel: registers to spare, fetch early
@@ -962,13 +966,15 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           Real fl[5], unused[5];
           face_fluxes<Real, NQ, false>(P, own, nb[0], 0, fl, unused);
           const Real lift = P.lift[dir];
-          Real* rec = P.frec + ((eg * 3 + f) * 5) * FP + l;
+          Real* rec = P.frec + (f * P.ne + eg) * FB + l;
 #pragma unroll
-          for (int v = 0; v < 5; ++v) rec[v * FP] = lift * fl[v];
+          for (int v = 0; v < 5; ++v) rec[v * N2] = lift * fl[v];
         }
       }
-      // these slots are read through cp.async by other threads of the group
+      // these slots are read back by a bulk copy (async proxy) one thread issues
+      __threadfence();
       __syncthreads();
+      if (tid == 0) asm volatile("fence.proxy.async;" ::: "memory");
     }
   } else {
     __syncthreads();
@@ -1002,9 +1008,9 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         face_fluxes<Real, NQ, true>(P, own, nb[0], 1, flo, fln);
         const Real lift = P.lift[dir];
         if (roles & (8u << dir)) {
-          Real* rec = P.frec + ((static_cast<long long>(code) * 3 + dir) * 5) * FP + l;
+          Real* rec = P.frec + (dir * P.ne + code) * FB + l;
 #pragma unroll
-          for (int v = 0; v < 5; ++v) rec[v * FP] = lift * fln[v];
+          for (int v = 0; v < 5; ++v) rec[v * N2] = lift * fln[v];
         }
         Real* tn = tslab + (1 + dir) * TV;
         Real* tt1 = tslab + (1 + d1) * TV;
@@ -1102,6 +1108,20 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
 #pragma unroll 1
 #endif
     for (int dir = 0; dir < 3; ++dir) {
+#ifdef ESDG_X_NO_PULL_TMA
+      if (false) {
+#else
+      if (SURF && tid == 0) {
+#endif
+        // the landing area is free: a barrier ended phase C / the previous
+        // direction, whose pulled values every thread has taken out by then
+        const long long left = P.ne - e0;
+        const unsigned nel = left < EPB ? unsigned(left) : unsigned(EPB);
+        const unsigned bytes = nel * FB * unsigned(sizeof(Real));
+        fence_proxy_async_smem(); // generic-proxy reads of the area -> the copy's writes
+        mbar_expect_tx(mbar, bytes);
+        bulk_g2s(pbuf, P.frec + (dir * P.ne + e0) * FB, bytes, mbar);
+      }
       if (active) {
         const int base = dir == 0 ? e * N3P + PX * l
                                   : (dir == 1 ? e * N3P + l0 + ZS * l1 : zbase);
@@ -1111,19 +1131,12 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
 #pragma unroll
           for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
         // One-pass kernels, "pulls": the lift term of the - face this line
-        // starts on (lf = 2 dir) lies in the element's slot of frec -- pushed
+        // starts on (lf = 2 dir) lies in the element's block of frec -- pushed
         // by the element across the face during its phase C, or put there by
-        // this group after phase A. The thread that sweeps a line is the face
-        // node (s, t) of the line's two faces: (l0, l1), for y lines (l1, l0).
-        // Asynchronous copies fetch the five values into shared memory while
-        // the pair fluxes are evaluated: no register is held for them and
-        // nobody waits for L2.
-        Real* slot = nullptr;
-        if (SURF) {
-          slot = P.frec + ((eg * 3 + dir) * 5) * FP + (dir == 1 ? l1 + NQ * l0 : l);
-#pragma unroll
-          for (int v = 0; v < 5; ++v) cp_async<sizeof(Real)>(&pbuf[v * T + tid], slot + v * FP);
-        }
+        // this group after phase A. One bulk copy (issued below, before the
+        // line loads of all threads) brings the group's blocks of this
+        // direction into shared memory while the pair fluxes are evaluated:
+        // no register, no load/store-pipe instruction, nobody waits for L2.
         // x and y lines of a Cartesian mesh see a constant potential: no
         // gravity term there (a second, shorter code instance of the sweep)
         if (FlatXY<NQ, sizeof(Real)>::value && SURF && P.flat_phi && dir < 2)
@@ -1132,17 +1145,26 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           sweep_line<Real, NQ, !(VOL && SURF), false>(P, vals, VS, base, stride, dir, acc);
         Real pull[5];
         if (SURF) {
-          cp_async_wait_all();
+          // The thread that sweeps a line is the face node (s, t) of the
+          // line's two faces: (l0, l1), for y lines (l1, l0).
+          const int fn = dir == 1 ? l1 + NQ * l0 : l;
+          Real* slot = P.frec + (dir * P.ne + eg) * FB + fn;
+#ifndef ESDG_X_NO_PULL_WAIT
+          mbar_wait(mbar, (dir + 1) & 1);
+#endif
           bool filled = true;
 #pragma unroll
           for (int v = 0; v < 5; ++v) {
-            pull[v] = pbuf[v * T + tid];
+            pull[v] = pbuf[e * FB + v * N2 + fn];
             filled = filled && !is_unfilled(pull[v]);
           }
+#ifdef ESDG_X_NO_PULL_WAIT
+          filled = true;
+#endif
           if (!filled) {
 #pragma unroll 1
             for (int v = 0; v < 5; ++v) {
-              const Real x = wait_filled(slot + v * FP, P.sync_error);
+              const Real x = wait_filled(slot + v * N2, P.sync_error);
               pull[0] = v == 0 ? x : pull[0];
               pull[1] = v == 1 ? x : pull[1];
               pull[2] = v == 2 ? x : pull[2];
@@ -1152,7 +1174,9 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           }
           // the slot is empty again for the next evaluation
 #pragma unroll
-          for (int v = 0; v < 5; ++v) set_unfilled(slot + v * FP);
+#ifndef ESDG_X_NO_PULL_RESET
+          for (int v = 0; v < 5; ++v) set_unfilled(slot + v * N2);
+#endif
           if (dir == 2) {
 #pragma unroll
             for (int v = 0; v < 5; ++v) pull_z[v] = pull[v];

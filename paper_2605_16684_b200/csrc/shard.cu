@@ -634,10 +634,11 @@ private:
     }
     CU(alloc_copy(&roles_all_, roles[0].data(), size_t(ne_)));
     CU(alloc_copy(&roles_split_, roles[1].data(), size_t(ne_)));
-    // slots of the pushed lift terms, all "not filled" (an all-ones NaN): rows
-    // padded to whole 128-byte lines (dev::FrecPitch)
+    // blocks of the pushed lift terms, [3][element][5 n2 Reals padded to 16
+    // bytes] (dev::FrecBlock), all "not filled" (an all-ones NaN); + 64: the
+    // bulk copy of a group's blocks may be issued for the last, partial group
     const size_t frec_bytes =
-        sizeof(Real) * size_t(std::max<int64_t>(ne_, 1)) * 15 * size_t((n2_ + 15) & ~15);
+        size_t(std::max<int64_t>(ne_, 1)) * 3 * ((sizeof(Real) * 5 * size_t(n2_) + 15) & ~size_t(15)) + 64;
     CU(cudaMalloc(&frec_, frec_bytes));
     CU(cudaMemset(frec_, 0xff, frec_bytes));
     interior.insert(interior.end(), boundary.begin(), boundary.end());
