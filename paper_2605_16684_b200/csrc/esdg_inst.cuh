@@ -8,7 +8,7 @@ namespace esdg_b200 {
 
 namespace {
 constexpr int kMaxDevices = 64;
-template <class Real, int NQ, bool VOL, bool SURF>
+template <class Real, int NQ, bool VOL, bool SURF, int RUNG = dev::kRungProduct>
 cudaError_t launch_one(const dev::RhsParams<Real, NQ>& P, long long n_groups,
                        cudaStream_t stream) {
   constexpr int EPB = dev::Tile<NQ, sizeof(Real)>::EPB;
@@ -18,7 +18,7 @@ cudaError_t launch_one(const dev::RhsParams<Real, NQ>& P, long long n_groups,
 #define ESDG_TUNE_EXTRA_SMEM 0
 #endif
   constexpr size_t smem = dev::SmemMap<Real, NQ, EPB>::kBytes + ESDG_TUNE_EXTRA_SMEM;
-  auto kern = dev::rhs_kernel<Real, NQ, EPB, MINB, VOL, SURF>;
+  auto kern = dev::rhs_kernel<Real, NQ, EPB, MINB, VOL, SURF, RUNG>;
   // the opt-in is a property of the (kernel, device) pair: once per device
   static std::atomic<bool> opted[kMaxDevices];
   int device = 0;
@@ -38,6 +38,22 @@ cudaError_t launch_one(const dev::RhsParams<Real, NQ>& P, long long n_groups,
 }
 } // namespace
 
+#ifdef ESDG_INST_LADDER
+template <class Real, int NQ>
+cudaError_t launch_ladder(int rung, const dev::RhsParams<Real, NQ>& P, cudaStream_t stream) {
+  switch (rung) {
+    case dev::kRungRecompute:
+      return launch_one<Real, NQ, true, false, dev::kRungRecompute>(P, 0, stream);
+    case dev::kRungPrecompute:
+      return launch_one<Real, NQ, true, false, dev::kRungPrecompute>(P, 0, stream);
+    case dev::kRungLogMean:
+      return launch_one<Real, NQ, true, false, dev::kRungLogMean>(P, 0, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+#define ESDG_INSTANTIATE(REAL, NQ)                                             \
+  template cudaError_t launch_ladder<REAL, NQ>(int, const dev::RhsParams<REAL, NQ>&, cudaStream_t);
+#else
 template <class Real, int NQ>
 cudaError_t launch_rhs(int mode, const dev::RhsParams<Real, NQ>& P,
                        long long n_groups, cudaStream_t stream) {
@@ -77,6 +93,8 @@ void rhs_launch_shape(int* threads, int* epb, size_t* smem_bytes) {
                                              const int32_t*, REAL*, long long, \
                                              cudaStream_t);                    \
   template void rhs_launch_shape<REAL, NQ>(int*, int*, size_t*);
+
+#endif // ESDG_INST_LADDER
 
 ESDG_INSTANTIATE(double, ESDG_NQ)
 ESDG_INSTANTIATE(float, ESDG_NQ)

@@ -388,10 +388,11 @@ __device__ __forceinline__ Node<Real> rotate_node(const Real nv[V_COUNT],
 // FP64 pipe for three cycles instead of two). One code instance
 // serves the three directions (the instruction cache is a real constraint
 // for these fully unrolled bodies).
-template <class Real, int NQ, bool DIAG, bool FLAT>
+template <class Real, int NQ, bool DIAG, bool FLAT, int RUNG = kRungProduct>
 __device__ __forceinline__ void sweep_line(const RhsParams<Real, NQ>& P,
                                            const Real* vals, int VS, int base,
-                                           int stride, int dir, Real (&acc)[NQ][5]) {
+                                           int stride, int dir, Real (&acc)[NQ][5],
+                                           const Real* logtab = nullptr) {
   // At the highest orders a line's node values and accumulators (14 NQ
   // Reals) no longer fit the register file next to the flux temporaries.
   // There only the five quantities every pair uses twice stay resident;
@@ -432,67 +433,58 @@ __device__ __forceinline__ void sweep_line(const RhsParams<Real, NQ>& P,
       for (int v = 0; v < 5; ++v) acc[i][v] = fma_(cii, f[v], acc[i][v]);
     }
   }
-#ifdef ESDG_LADDER_NO_SYMMETRY
-  // Ladder rungs below the product (the reference's optimisation ladder,
-  // kernels.hpp:20-34, ladder.hpp:28-82), build-time switches for the
-  // measurement in profiles/r1_ladder.txt; the product always uses the
-  // symmetric sweep below.
-  //   ESDG_LADDER_NO_SYMMETRY  every ORDERED pair is evaluated and only node i
-  //                            is updated (the "precompute"/"logmean" rungs)
-  //   + ESDG_LADDER_RECOMPUTE  primitives and both logarithms are worked out
-  //                            again inside every flux evaluation, for both
-  //                            nodes (the "baseline"/"fused" rungs:
-  //                            compute_node_vals per evaluation, 2 div + 2 log)
-  //   ESDG_LADDER_IEEE_DIV     (esdg_device.cuh) library division instead of
-  //                            the seed + one cubic step reciprocal
-#ifdef ESDG_LADDER_RECOMPUTE
-  extern __shared__ __align__(16) unsigned char ladder_smem[];
-  const Real* ladder_tab = reinterpret_cast<const Real*>(
-      ladder_smem + SmemMap<Real, NQ, Tile<NQ, sizeof(Real)>::EPB>::kTab);
-  auto again = [&](const Node<Real>& n, Real tie) {
-    // conservative variables back from the parked quantities, then
-    // compute_node_vals (physics.hpp:56-80) once more. The exact zero times
-    // a value of the partner (`tie`, a different one in the two roles) binds
-    // the recomputation to this evaluation; the compiler would otherwise
-    // merge the recomputations of one node.
-    const Real rho = fma_(Real(0), tie, n.hr + n.hr);
-    const Real m1 = rho * n.hun, m2 = rho * n.hut1, m3 = rho * n.hut2; // momenta / 2
-    const Real p = rho * n.hib;                                          // rho / (2 b)
-    const Real inv = rcp_(rho);
-    Node<Real> r;
-    r.hr = Real(0.5) * rho;
-    r.hun = m1 * inv;
-    r.hut1 = m2 * inv;
-    r.hut2 = m3 * inv;
-    r.b = rho * rcp_(p + p);
-    r.hib = p * inv;
-    r.hlr = Real(0.5) * log_(rho, ladder_tab);
-    r.lb = log_(r.b, ladder_tab);
-    r.hphi = n.hphi;
-    return r;
-  };
-#endif
+  if constexpr (RUNG < kRungProduct) {
+    // Ladder rungs below the product (esdg_device.cuh, kRung*): every ORDERED
+    // pair is evaluated and only node i is updated. kRungRecompute works out
+    // primitives and both logarithms again inside every flux evaluation, for
+    // both nodes (compute_node_vals per evaluation: 2 div + 2 log each).
+    constexpr bool kIeee = RUNG < kRungLogMean;
+    auto again = [&](const Node<Real>& n, Real tie) {
+      // conservative variables back from the parked quantities, then
+      // compute_node_vals (physics.hpp:56-80) once more. The exact zero times
+      // a value of the partner (`tie`, a different one in the two roles) binds
+      // the recomputation to this evaluation; the compiler would otherwise
+      // merge the recomputations of one node.
+      const Real rho = fma_(Real(0), tie, n.hr + n.hr);
+      const Real m1 = rho * n.hun, m2 = rho * n.hut1, m3 = rho * n.hut2; // momenta / 2
+      const Real p = rho * n.hib;                                          // rho / (2 b)
+      const Real inv = rcpx<kIeee>(rho);
+      Node<Real> r;
+      r.hr = Real(0.5) * rho;
+      r.hun = m1 * inv;
+      r.hut1 = m2 * inv;
+      r.hut2 = m3 * inv;
+      r.b = rho * rcpx<kIeee>(p + p);
+      r.hib = p * inv;
+      r.hlr = Real(0.5) * log_(rho, logtab);
+      r.lb = log_(r.b, logtab);
+      r.hphi = n.hphi;
+      return r;
+    };
 #pragma unroll
-  for (int i = 0; i < NQ; ++i) {
+    for (int i = 0; i < NQ; ++i) {
 #pragma unroll
-    for (int j = 0; j < NQ; ++j) {
-      if (j == i) continue;
-#ifdef ESDG_LADDER_RECOMPUTE
-      const PairFlux<Real> pf = pair_flux(again(nd[i], nd[j].hphi), again(nd[j], nd[i].hun), P.gas.cg);
-#else
-      const PairFlux<Real> pf = pair_flux(nd[i], nd[j], P.gas.cg);
-#endif
-      const Real cij = P.negd[i * NQ + j];
-      const Real fni = fma_(pf.tg, nd[i].hib, pf.f[1]);
-      acc[i][0] = fma_(cij, pf.f[0], acc[i][0]);
-      acc[i][1] = fma_(cij, fni, acc[i][1]);
-      acc[i][2] = fma_(cij, pf.f[2], acc[i][2]);
-      acc[i][3] = fma_(cij, pf.f[3], acc[i][3]);
-      acc[i][4] = fma_(cij, pf.f[4], acc[i][4]);
+      for (int j = 0; j < NQ; ++j) {
+        if (j == i) continue;
+        cold(i);
+        cold(j);
+        PairFlux<Real> pf;
+        if constexpr (RUNG <= kRungRecompute)
+          pf = pair_flux<Real, false, kIeee>(again(nd[i], nd[j].hphi), again(nd[j], nd[i].hun),
+                                             P.gas.cg);
+        else
+          pf = pair_flux<Real, false, kIeee>(nd[i], nd[j], P.gas.cg);
+        const Real cij = P.negd[i * NQ + j];
+        const Real fni = fma_(pf.tg, nd[i].hib, pf.f[1]);
+        acc[i][0] = fma_(cij, pf.f[0], acc[i][0]);
+        acc[i][1] = fma_(cij, fni, acc[i][1]);
+        acc[i][2] = fma_(cij, pf.f[2], acc[i][2]);
+        acc[i][3] = fma_(cij, pf.f[3], acc[i][3]);
+        acc[i][4] = fma_(cij, pf.f[4], acc[i][4]);
+      }
     }
+    return;
   }
-  return;
-#endif
   // off-diagonal pairs, each once (kernels.hpp:190-231). FLAT: phi is the
   // same at every node of this line (see pair_flux), the gravity term
   // vanishes identically and <phi> is the line's phi.
@@ -723,9 +715,10 @@ __device__ __noinline__ Real wait_filled(const Real* src, unsigned long long* sy
   return x;
 }
 
-template <class Real, int NQ, int EPB, int MINB, bool VOL, bool SURF>
+template <class Real, int NQ, int EPB, int MINB, bool VOL, bool SURF, int RUNG = kRungProduct>
 __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     rhs_kernel(const __grid_constant__ RhsParams<Real, NQ> P) {
+  static_assert(RUNG == kRungProduct || (VOL && !SURF), "ladder rungs are volume kernels");
   using G = Geo<NQ>;
   constexpr int N2 = G::N2, N3 = G::N3, PX = G::PX, N3P = G::N3P;
   constexpr int VS = EPB * N3P; // stride between quantity arrays
@@ -914,7 +907,8 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     // iteration loop has a fifth of the code but measured 3-6 % slower). A
     // non-physical node is only remembered here and reported after the loop.
     Real nvs[NQ][V_COUNT], prs[NQ];
-    const unsigned badmask = node_vals_line<Real, NQ>(qv, ph, P.gas.gm1, logtab, nvs, prs);
+    const unsigned badmask =
+        node_vals_line<Real, NQ, (RUNG < kRungLogMean)>(qv, ph, P.gas.gm1, logtab, nvs, prs);
 #pragma unroll
     for (int k = 0; k < NQ; ++k) {
       const int s = zbase + k * ZS;
@@ -1142,7 +1136,8 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         if (FlatXY<NQ, sizeof(Real)>::value && SURF && P.flat_phi && dir < 2)
           sweep_line<Real, NQ, !(VOL && SURF), true>(P, vals, VS, base, stride, dir, acc);
         else
-          sweep_line<Real, NQ, !(VOL && SURF), false>(P, vals, VS, base, stride, dir, acc);
+          sweep_line<Real, NQ, !(VOL && SURF), false, RUNG>(P, vals, VS, base, stride, dir, acc,
+                                                            logtab);
         Real pull[5];
         if (SURF) {
           // The thread that sweeps a line is the face node (s, t) of the

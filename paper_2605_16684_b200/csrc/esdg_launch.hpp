@@ -22,6 +22,11 @@ template <class Real, int NQ>
 cudaError_t launch_rhs(int mode, const dev::RhsParams<Real, NQ>& P,
                        long long n_groups, cudaStream_t stream);
 
+// Volume kernel of a ladder rung below the product (dev::kRungRecompute,
+// kRungPrecompute, kRungLogMean; inst_ladder_nq*.cu), all elements.
+template <class Real, int NQ>
+cudaError_t launch_ladder(int rung, const dev::RhsParams<Real, NQ>& P, cudaStream_t stream);
+
 template <class Real, int NQ>
 cudaError_t launch_pack(const Real* q, const int32_t* send_elem,
                         const int32_t* send_face, Real* send, long long n_send,

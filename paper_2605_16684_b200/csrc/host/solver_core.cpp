@@ -281,6 +281,7 @@ int SolverCore::set_variant(int variant) {
     return ESDG_B200_BADARG;
   }
   variant_ = variant;
+  for (auto& ls : shards_) ls.dev->set_variant(variant);
   return ESDG_B200_OK;
 }
 
@@ -684,7 +685,9 @@ int SolverCore::rhs(int src, int dst, double a_old, double a_new,
   const bool halo = any_halo_ && !volume_only;
   const int source = (with_source && opt_.settings.coriolis_mode != 0) ? 1 : 0;
   if (halo) RC(exchange_begin(src));
-  if (path_ != ESDG_B200_PATH_SPLIT && !volume_only) {
+  // rungs of the ladder below "symmetric" exist as volume kernels only: the
+  // split structure serves them whatever the path
+  if (path_ != ESDG_B200_PATH_SPLIT && !volume_only && variant_ >= 4) {
     // one-pass kernel: the element groups without a ghost face run while the
     // traces travel, the others after they have landed (solver.hpp:259-294)
     const bool split = halo && overlap_;

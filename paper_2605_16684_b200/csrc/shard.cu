@@ -301,6 +301,7 @@ public:
   int64_t launch_count() const override { return launches_; }
   void set_dissipation(int on) override { dissipation_ = on; }
   void set_face_sharing(int on) override { share_faces_ = on; }
+  void set_variant(int variant) override { variant_ = variant; }
 
   int pack(int src, cudaStream_t st) override {
     if (src != 0 && src != 1) return bad("pack: bad register");
@@ -577,6 +578,12 @@ private:
     P.face_roles = share ? (groups ? roles_split_ : roles_all_) : nullptr;
     P.frec = frec_;
     P.sync_error = flag_ + 1;
+    if (mode == kModeVolume && variant_ < 4 && !groups && n_groups == 0) {
+      // a rung of the reference's ladder below "symmetric" (kernels.hpp:20-34)
+      const int rung = variant_ <= 1 ? dev::kRungRecompute
+                                     : (variant_ == 2 ? dev::kRungPrecompute : dev::kRungLogMean);
+      return launch_ladder<Real, NQ>(rung, P, st);
+    }
     return launch_rhs<Real, NQ>(mode, P, n_groups, st);
   }
 
@@ -715,6 +722,7 @@ private:
   uint8_t *roles_all_ = nullptr, *roles_split_ = nullptr;
   Real* frec_ = nullptr;
   int share_faces_ = 1;
+  int variant_ = 5; // KernelVariant::Balanced
   int epb_ = 1;
   unsigned long long *flag_ = nullptr, *flag_host_ = nullptr;
   double *red_out_ = nullptr, *red_tab_ = nullptr;

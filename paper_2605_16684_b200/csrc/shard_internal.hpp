@@ -30,6 +30,9 @@ public:
   virtual int64_t launch_count() const = 0;
   virtual void set_dissipation(int on) = 0;
   virtual void set_face_sharing(int on) = 0;
+  // KernelVariant 0..5 (kernels.hpp:27-34): rungs below 4 run a ladder instance
+  // of the volume kernel
+  virtual void set_variant(int variant) = 0;
   virtual int pack(int src, cudaStream_t st) = 0;
   // mode: RhsMode (esdg_launch.hpp); part: ESDG_B200_PART_* -- all elements,
   // or only the element groups without / with a ghost face
