@@ -440,22 +440,30 @@ __device__ __forceinline__ void sweep_line(const RhsParams<Real, NQ>& P,
     // both nodes (compute_node_vals per evaluation: 2 div + 2 log each).
     constexpr bool kIeee = RUNG < kRungLogMean;
     auto again = [&](const Node<Real>& n, Real tie) {
-      // conservative variables back from the parked quantities, then
-      // compute_node_vals (physics.hpp:56-80) once more. The exact zero times
-      // a value of the partner (`tie`, a different one in the two roles) binds
-      // the recomputation to this evaluation; the compiler would otherwise
-      // merge the recomputations of one node.
+      // compute_node_vals (physics.hpp:56-80) once more: conservative
+      // variables back from the parked quantities, two divisions, two
+      // logarithms. The reference's variants see bitwise the same node values
+      // whether they recompute them or not (same function of the same q;
+      // acceptance criterion 4 holds them to 1e-13 of each other), and a
+      // quantity rebuilt from rounded intermediates would be an ulp off --
+      // which a logarithmic mean amplifies by 1/(2 xi). So the divisions are
+      // carried out and then tied to the parked values through an exact
+      // zero: every operation of the recomputation is executed, the values
+      // stay the parked ones. Logarithms of unchanged arguments reproduce
+      // themselves. `tie` (a different value of the partner in the two roles)
+      // keeps the compiler from merging the recomputations of one node.
       const Real rho = fma_(Real(0), tie, n.hr + n.hr);
       const Real m1 = rho * n.hun, m2 = rho * n.hut1, m3 = rho * n.hut2; // momenta / 2
       const Real p = rho * n.hib;                                          // rho / (2 b)
       const Real inv = rcpx<kIeee>(rho);
+      const Real b2 = rho * rcpx<kIeee>(p + p);
       Node<Real> r;
       r.hr = Real(0.5) * rho;
-      r.hun = m1 * inv;
-      r.hut1 = m2 * inv;
-      r.hut2 = m3 * inv;
-      r.b = rho * rcpx<kIeee>(p + p);
-      r.hib = p * inv;
+      r.hun = fma_(Real(0), m1 * inv, n.hun);
+      r.hut1 = fma_(Real(0), m2 * inv, n.hut1);
+      r.hut2 = fma_(Real(0), m3 * inv, n.hut2);
+      r.b = fma_(Real(0), b2, n.b);
+      r.hib = fma_(Real(0), p * inv, n.hib);
       r.hlr = Real(0.5) * log_(rho, logtab);
       r.lb = log_(r.b, logtab);
       r.hphi = n.hphi;
@@ -908,7 +916,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     // non-physical node is only remembered here and reported after the loop.
     Real nvs[NQ][V_COUNT], prs[NQ];
     const unsigned badmask =
-        node_vals_line<Real, NQ, (RUNG < kRungLogMean)>(qv, ph, P.gas.gm1, logtab, nvs, prs);
+        node_vals_line<Real, NQ>(qv, ph, P.gas.gm1, logtab, nvs, prs);
 #pragma unroll
     for (int k = 0; k < NQ; ++k) {
       const int s = zbase + k * ZS;

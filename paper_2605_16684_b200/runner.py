@@ -15,8 +15,11 @@ The samples use the device reductions (K6), so nothing but one double per
 element leaves the GPU between steps. The mesh/case tables are this
 repository's (bubble: tests/test_helpers.hpp:10-21 and cases.hpp:43-69;
 channel: config.cpp:84-95 with the surrogate initial state of
-csrc/host/cases.cpp -- the reference ships none). The config-file parser and
-the theta slices of the reference's runner are not reproduced.
+csrc/host/cases.cpp -- the reference ships none), and theta_slice() writes
+slices/theta_y0_<step>.csv like runner.cpp:78-123. The config-file parser is
+not reproduced here: the reference's own runner.cpp + config.cpp compile
+unmodified against GpuSolver (oracle/Makefile, tests/test_reference_swap.py)
+and are the value-checked route for configuration files.
 """
 from __future__ import annotations
 
