@@ -279,6 +279,17 @@ template <int E, int M> struct TilePick { static constexpr int EPB = E, MINB = M
 // uses it, and only in the one-pass kernels (the volume-only kernel at N=6
 // loses 16 % with it).
 template <int NQ, int BYTES> struct FlatXY { static constexpr bool value = NQ == 7; };
+// SHARE: the one-pass kernels evaluate every interior face once and hand the
+// other element its lift term through RhsParams::frec. It pays where the face
+// phase was the long, badly overlapped part of a CTA's life (N <= 5, N = 7 in
+// FP64: +3 ... +10 % on the stage path) and loses where one or two fat CTAs
+// per SM ran the six faces as paired instruction streams (FPI = 2): there
+// halving the faces halves the work per iteration, not the latency of an
+// iteration (N = 6 FP64 -6 %, N = 7 FP32 -7 %); those tiles keep evaluating
+// all six faces of an element.
+template <int NQ, int BYTES> struct Share { static constexpr bool value = true; };
+template <> struct Share<7, 8> { static constexpr bool value = false; };
+template <> struct Share<8, 4> { static constexpr bool value = false; };
 template <> struct Tile<6, 8> : TilePick<ESDG_TUNE_T68E, ESDG_TUNE_T68M> { static constexpr int FPI = 2; static constexpr bool LEAN = false; };
 template <> struct Tile<7, 8> : TilePick<ESDG_TUNE_T78E, ESDG_TUNE_T78M> { static constexpr int FPI = 2; static constexpr bool LEAN = true; };
 template <> struct Tile<8, 8> { static constexpr int EPB = 1, MINB = 3; static constexpr int FPI = 2; static constexpr bool LEAN = true; };
@@ -783,13 +794,14 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
 
   // the one-pass kernels keep the codes of the + faces only (the sweeps
   // evaluate those); the - faces are looked at once, right before the commit
+  constexpr bool kShare = VOL && SURF && Share<NQ, sizeof(Real)>::value;
   int codes[6] = {-1, -1, -1, -1, -1, -1};
   unsigned roles = 0;
   if (SURF && active) {
 #pragma unroll
     for (int lf = 0; lf < 6; ++lf)
-      if (!VOL || (lf & 1)) codes[lf] = P.nbr[eg * 6 + lf];
-    if (VOL && P.face_roles) roles = P.face_roles[eg];
+      if (!kShare || (lf & 1)) codes[lf] = P.nbr[eg * 6 + lf];
+    if (kShare && P.face_roles) roles = P.face_roles[eg];
   }
 
   // Neighbour state of face lf, fetched one face ahead of its use so the
@@ -924,10 +936,15 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     }
     const int bad = badmask ? __ffs(badmask) - 1 : -1;
     if (SURF && VOL) {
-      // the trace across the first face the sweeps will evaluate: issued
+      // the trace(s) across the first face(s) phase C will evaluate: issued
       // here, not before the logarithms (registers the fused kernel's node
-      // loop cannot spare); it lands while the CTA gathers at the barrier
-      fetch(1, cur[0]);
+      // loop cannot spare); they land while the CTA gathers at the barrier
+      if (kShare) {
+        fetch(1, cur[0]);
+      } else {
+        fetch(0, cur[0]);
+        if (FPI == 2) fetch(1, cur[FPI - 1]);
+      }
     }
     if (bad >= 0) {
       const Real* qb = qe + bad * N2;
@@ -941,7 +958,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   }
   ESDG_CLK();
   cp_async_wait_all(); // this thread's share of out_old is in the slab
-  if (VOL && SURF) {
+  if (kShare) {
     // One-pass kernels: - faces (lf even) that no other element evaluates for
     // this one -- walls, ghost faces, neighbours that come later in the launch
     // order. Thread (l0, l1) is face node (s, t) = (l0, l1); the lift term
@@ -987,7 +1004,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // Every face subtracts its lift term from the shared tendency slab (zeroed
   // by the z-line owners in phase A). Faces of one direction share no node,
   // faces of different directions do (edges), hence the two barriers.
-  if (SURF && VOL) {
+  if (kShare) {
     // One-pass kernels: only the three + faces (lf = 1, 3, 5) are evaluated
     // here, for both elements they separate: this element's lift term goes to
     // the slab, the other element's -- bitwise what it would compute itself,
@@ -1033,7 +1050,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
       __syncthreads();
     }
   }
-  if (SURF && !VOL) {
+  if (SURF && !kShare) {
     // FPI faces per iteration (Tile<>::FPI). 2 = both faces of a direction as
     // two interleaved instruction streams: more ILP, but twice the loop
     // body. Where three or more CTAs in different phases share an SM the
@@ -1110,11 +1127,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
 #pragma unroll 1
 #endif
     for (int dir = 0; dir < 3; ++dir) {
-#ifdef ESDG_X_NO_PULL_TMA
-      if (false) {
-#else
-      if (SURF && tid == 0) {
-#endif
+      if (kShare && tid == 0) {
         // the landing area is free: a barrier ended phase C / the previous
         // direction, whose pulled values every thread has taken out by then
         const long long left = P.ne - e0;
@@ -1147,23 +1160,18 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           sweep_line<Real, NQ, !(VOL && SURF), false, RUNG>(P, vals, VS, base, stride, dir, acc,
                                                             logtab);
         Real pull[5];
-        if (SURF) {
+        if (kShare) {
           // The thread that sweeps a line is the face node (s, t) of the
           // line's two faces: (l0, l1), for y lines (l1, l0).
           const int fn = dir == 1 ? l1 + NQ * l0 : l;
           Real* slot = P.frec + (dir * P.ne + eg) * FB + fn;
-#ifndef ESDG_X_NO_PULL_WAIT
           mbar_wait(mbar, (dir + 1) & 1);
-#endif
           bool filled = true;
 #pragma unroll
           for (int v = 0; v < 5; ++v) {
             pull[v] = pbuf[e * FB + v * N2 + fn];
             filled = filled && !is_unfilled(pull[v]);
           }
-#ifdef ESDG_X_NO_PULL_WAIT
-          filled = true;
-#endif
           if (!filled) {
 #pragma unroll 1
             for (int v = 0; v < 5; ++v) {
@@ -1177,9 +1185,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           }
           // the slot is empty again for the next evaluation
 #pragma unroll
-#ifndef ESDG_X_NO_PULL_RESET
           for (int v = 0; v < 5; ++v) set_unfilled(slot + v * N2);
-#endif
           if (dir == 2) {
 #pragma unroll
             for (int v = 0; v < 5; ++v) pull_z[v] = pull[v];
@@ -1212,7 +1218,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
             for (int i = 0; i < NQ; ++i)
 #pragma unroll
               for (int v = 0; v < 5; ++v) acc[i][v] = fma_(scale, acc[i][v], old[i][v]);
-            if (SURF) {
+            if (kShare) {
               // the - face at the line's first node, same rotated frame
 #pragma unroll
               for (int v = 0; v < 5; ++v) acc[0][v] = fma_(-P.gain, pull[v], acc[0][v]);
@@ -1292,7 +1298,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         knew[k][3] = fma_(zscale, acc[k][1], knew[k][3]);
         knew[k][4] = fma_(zscale, acc[k][4], knew[k][4]);
       }
-      if (SURF) {
+      if (kShare) {
         // the - z face at the line's first node (normal -> var 3, x, y)
         knew[0][0] = fma_(-P.gain, pull_z[0], knew[0][0]);
         knew[0][3] = fma_(-P.gain, pull_z[1], knew[0][3]);
