@@ -292,9 +292,19 @@ def main_b200(args, rank, local_rank, world):
         if rank == 0:
             uid.copy_(torch.frombuffer(bytearray(capi.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, 0)
-        solver = capi.GpuSolver(mesh, args.order, args.precision, settings=settings,
-                                nccl=(world, rank, device, bytes(uid.cpu().numpy().tobytes())))
-    elif world > 1:
+        solver = None
+        try:
+            solver = capi.GpuSolver(mesh, args.order, args.precision, settings=settings,
+                                    nccl=(world, rank, device, bytes(uid.cpu().numpy().tobytes())))
+        except Exception as exc:  # noqa: BLE001 -- every rank must take the same way out
+            print(f"[bench] rank {rank}: library-side NCCL exchange unavailable ({exc})", file=sys.stderr)
+        ok = torch.tensor([1 if solver is not None else 0], dtype=torch.int32, device=f"cuda:{device}")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            # fall back to the torch.distributed callback on all ranks alike
+            solver = None
+            args.exchange = "torch"
+    if world > 1 and args.exchange == "torch":
         from paper_2605_16684_b200 import halo
         solver = capi.GpuSolver(mesh, args.order, args.precision, settings=settings,
                                 distributed=(world, rank, device))
