@@ -38,7 +38,8 @@ for order, prec, case, path in points:
             key = "update"
         else:
             args = name[name.find("<") + 1:name.rfind(">")].replace("(bool)", "").replace("(int)", "").split(",")
-            vol, surf = args[-2].strip() in ("1", "true"), args[-1].strip() in ("1", "true")
+            # rhs_kernel<Real, NQ, EPB, MINB, VOL, SURF, RUNG>
+            vol, surf = args[4].strip() in ("1", "true"), args[5].strip() in ("1", "true")
             key = path if (vol and surf) else ("volume" if vol else "surface")
         groups.setdefault(key, []).append(b)
     for key, vals in groups.items():

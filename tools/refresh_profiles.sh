@@ -24,19 +24,4 @@ csv.writer(open('/tmp/k1_source.csv', 'w')).writerows(out)
 PY
 (echo "stage kernel:"; python tools/ncu_fp64_cycles.py gpurun_out/${TAG}_full_stage_source.csv; python tools/ncu_stalls.py gpurun_out/${TAG}_full_stage_source.csv
  echo; echo "split path, volume kernel:"; python tools/ncu_fp64_cycles.py /tmp/k1_source.csv; python tools/ncu_stalls.py /tmp/k1_source.csv) > profiles/${TAG}_ncu_stage_pipe_cycles.txt
-python - <<PY
-import csv, io, json, subprocess
-out = {}
-for rep, keys in (("gpurun_out/${TAG}_full_stage.ncu-rep", ["stage"]), ("gpurun_out/${TAG}_full_split.ncu-rep", ["volume", "surface", "update"])):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(txt)))
-    hdr, units = rows[0], rows[1]
-    for k, r in zip(keys, rows[2:]):
-        def val(name):
-            v = float(r[hdr.index(name)].replace(",", ""))
-            return v * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}.get(units[hdr.index(name)], 1)
-        out[k] = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
-out["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full at BASELINE.json "
-                "configs[1] (N=4, 884736 elements, FP64), see ${TAG}_ncu_full_summary.txt")
-json.dump(out, open("profiles/traffic.json", "w"), indent=1)
-PY
+# profiles/traffic.json comes from tools/collect_traffic.py (one ncu pass per sweep point)
