@@ -262,6 +262,17 @@ int esdg_b200_partition(int64_t n_elements, int ranks, int64_t* range_begin);
 int esdg_b200_exchange_plan(esdg_b200_mesh* m, int ranks, int32_t* ghost_count,
                             int32_t* interior_count,
                             esdg_b200_ghost_face* ghosts, int32_t* interior);
+/* Host-only: the face roles of the one-pass kernels for a shard with the
+ * neighbour codes nbr_local [n_elements][6] (as in esdg_b200_shard_desc) and
+ * elements_per_group consecutive elements per CTA (esdg_b200_rhs_launch_shape).
+ * roles[e]: bit f (0..2) = the lift term of face lf = 2f of e is pushed by the
+ * element across it, bit 3+d = e pushes the term of its face lf = 2d+1. split
+ * != 0: the table for the interior / boundary list launches (no sharing
+ * between a group with and a group without a ghost face). Every interior face
+ * keeps exactly one evaluator: the reference's one record per face
+ * (compute_face_record, kernels.hpp:350-384). */
+int esdg_b200_face_roles(const int32_t* nbr_local, int64_t n_elements,
+                         int elements_per_group, int split, uint8_t* roles);
 /* Host-only: the GPU-side slice of the exchange for partition `rank` of
  * `world_size`, i.e. exactly what esdg_b200_shard_create consumes. Ghost
  * faces are ordered by (peer, face) so that one contiguous block of traces

@@ -131,6 +131,7 @@ SIGNATURES = {
     "esdg_b200_solver_set_exchange_delay": (_i, [_vp, _i]),
     "esdg_b200_solver_destroy": (None, [_vp]),
     "esdg_b200_solver_set_path": (_i, [_vp, _i]),
+    "esdg_b200_face_roles": (_i, [_ip, _i64, _i, _i, _vp]),
     "esdg_b200_solver_set_overlap": (_i, [_vp, _i]),
     "esdg_b200_solver_set_face_sharing": (_i, [_vp, _i]),
     "esdg_b200_solver_overlap_elements": (_i, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
@@ -335,6 +336,17 @@ def rank_halo(mesh: Mesh, world_size: int, rank: int):
     return dict(begin=int(rb[rank]), end=int(rb[rank + 1]),
                 peers=[(int(peer[i]), int(off[i]), int(cnt[i])) for i in range(n)],
                 send_elem=se[:g].copy(), send_face=sf[:g].copy(), nbr_local=nbr)
+
+
+def face_roles(nbr_local, elements_per_group, split=False):
+    """Face roles of the one-pass kernels for a shard's neighbour codes (host
+    only): bit f = face lf = 2f is pulled, bit 3 + d = face lf = 2d + 1 is
+    pushed."""
+    nbr = np.ascontiguousarray(nbr_local, np.int32)
+    roles = np.zeros(max(1, nbr.shape[0]), np.uint8)
+    check(lib().esdg_b200_face_roles(nbr.ctypes.data_as(_ip), nbr.shape[0], int(elements_per_group),
+                                     1 if split else 0, roles.ctypes.data_as(_vp)))
+    return roles[:nbr.shape[0]]
 
 
 def reference_element(order):

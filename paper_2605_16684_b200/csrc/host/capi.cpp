@@ -247,6 +247,16 @@ void esdg_b200_solver_destroy(esdg_b200_solver* s) {
 
 #define CORE(s) if (!(s)) return ESDG_B200_BADARG; SolverCore& c = *(s)->core
 
+int esdg_b200_face_roles(const int32_t* nbr_local, int64_t n_elements, int elements_per_group,
+                         int split, uint8_t* roles) {
+  if (!nbr_local || !roles || n_elements < 0 || elements_per_group < 1) {
+    esdg_b200::set_message("face_roles: bad argument");
+    return ESDG_B200_BADARG;
+  }
+  esdg_b200::host::build_face_roles(nbr_local, n_elements, elements_per_group, split != 0, roles);
+  return ESDG_B200_OK;
+}
+
 int esdg_b200_solver_set_path(esdg_b200_solver* s, int path) { CORE(s); return c.set_path(path); }
 int esdg_b200_solver_set_variant(esdg_b200_solver* s, int variant) { CORE(s); return c.set_variant(variant); }
 int esdg_b200_solver_record_events(esdg_b200_solver* s, int on) { CORE(s); return c.record_events(on != 0); }

@@ -198,5 +198,23 @@ void build_rank_halo(const Mesh& m, const std::vector<int64_t>& rb, int r,
   }
 }
 
+void build_face_roles(const int32_t* nbr, int64_t ne, int epb, bool split, uint8_t* roles) {
+  const int64_t ng = (ne + epb - 1) / epb;
+  std::vector<uint8_t> boundary(size_t(ng), 0); // group has a ghost face
+  if (split)
+    for (int64_t e = 0; e < ne; ++e)
+      for (int lf = 0; lf < 6; ++lf)
+        if (nbr[e * 6 + lf] <= -2) boundary[size_t(e / epb)] = 1;
+  for (int64_t e = 0; e < ne; ++e) roles[e] = 0;
+  for (int64_t b = 0; b < ne; ++b)
+    for (int f = 0; f < 3; ++f) {
+      const int32_t a = nbr[b * 6 + 2 * f];
+      if (a < 0 || a >= b || nbr[int64_t(a) * 6 + 2 * f + 1] != int32_t(b)) continue;
+      if (split && boundary[size_t(a / epb)] != boundary[size_t(b / epb)]) continue;
+      roles[b] |= uint8_t(1u << f);
+      roles[a] |= uint8_t(8u << f);
+    }
+}
+
 } // namespace host
 } // namespace esdg_b200

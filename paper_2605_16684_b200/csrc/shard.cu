@@ -14,6 +14,7 @@
 #include "esdg_b200.h"
 #include "esdg_kernels.cuh"
 #include "esdg_launch.hpp"
+#include "host/host_types.hpp"
 #include "shard_internal.hpp"
 
 namespace esdg_b200 {
@@ -616,28 +617,11 @@ private:
     }
     n_groups_[0] = int64_t(interior.size());
     n_groups_[1] = int64_t(boundary.size());
-    // Face roles (RhsParams::face_roles). The face between A (its + face,
-    // lf odd) and B (its - face, lf - 1) is always evaluated by A. B takes
-    // A's result instead of evaluating the face a second time when A's group
-    // is dispatched no later than B's in the same launch: ascending group
-    // index for a launch over all groups (or over consecutive runs of them),
-    // and additionally the same list for the interior / boundary launches.
-    // Everything else -- walls, ghost faces, periodic wrap-around (A has the
-    // higher index there), faces between the two lists -- B evaluates itself.
-    std::vector<uint8_t> in_boundary(size_t(ng), 0);
-    for (int32_t g : boundary) in_boundary[size_t(g)] = 1;
+    // face roles of the one-pass kernels (host/mesh.cpp)
     std::vector<uint8_t> roles[2];
     for (int t = 0; t < 2; ++t) {
-      std::vector<uint8_t>& r = roles[t];
-      r.assign(size_t(ne_), 0);
-      for (int64_t b = 0; b < ne_; ++b)
-        for (int f = 0; f < 3; ++f) {
-          const int32_t a = nbr[b * 6 + 2 * f];
-          if (a < 0 || a >= b || nbr[int64_t(a) * 6 + 2 * f + 1] != int32_t(b)) continue;
-          if (t == 1 && in_boundary[size_t(a / epb)] != in_boundary[size_t(b / epb)]) continue;
-          r[size_t(b)] |= uint8_t(1u << f);
-          r[size_t(a)] |= uint8_t(8u << f);
-        }
+      roles[t].assign(size_t(std::max<int64_t>(ne_, 1)), 0);
+      host::build_face_roles(nbr, ne_, epb, t == 1, roles[t].data());
     }
     CU(alloc_copy(&roles_all_, roles[0].data(), size_t(ne_)));
     CU(alloc_copy(&roles_split_, roles[1].data(), size_t(ne_)));
