@@ -92,6 +92,7 @@ struct RhsParams {
   const uint8_t* face_roles;
   Real* frec;            // [3][element][FrecBlock<Real, NQ>]: slot f = face lf = 2f, [5][NQ^2] + pad
   unsigned long long* sync_error;
+  unsigned long long wait_limit_ns; // bound of a pull's poll (0: none), ESDG_B200_WAIT_LIMIT_MS
   int flat_phi;          // phi is constant along x and y lines (checked by the host)
   int prefetch_ctas;     // resident CTAs chip-wide: L2 prefetch distance
   int with_source;       // Coriolis on (commit_volume, solver.hpp:205-216)
@@ -720,17 +721,37 @@ __device__ __forceinline__ void set_unfilled(double* p) {
 __device__ __forceinline__ void set_unfilled(float* p) { *reinterpret_cast<int*>(p) = -1; }
 // A lift term that has not arrived although the element evaluating it was
 // dispatched before this one: poll L2 until it is there. The element that
-// pushes never waits for anybody, so this ends; the loop is bounded all the
-// same and a time-out is reported to the host instead of hanging the device.
+// pushes never waits for anybody, so this ends. The wait is bounded all the
+// same -- by wall time (RhsParams::wait_limit_ns on %globaltimer, 2 s unless the
+// environment says otherwise: a sanitizer or a debugger may slow
+// the pushing group down by orders of magnitude, an iteration count would
+// misfire there), and by the other waiters: the first one to give up raises
+// the error word, everybody else sees it and leaves, so a launch whose
+// dispatch order were ever violated ends within seconds and reports
+// ESDG_B200_CUDA instead of hanging the device.
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 template <class Real>
-__device__ __noinline__ Real wait_filled(const Real* src, unsigned long long* sync_error) {
+__device__ __noinline__ Real wait_filled(const Real* src, unsigned long long* sync_error,
+                                        unsigned long long limit_ns) {
   Real x = __ldcg(src);
+  if (!is_unfilled(x)) return x;
+  const unsigned long long t0 = global_ns();
 #pragma unroll 1
-  for (int spins = 0; is_unfilled(x) && spins < (1 << 15); ++spins) {
-    __nanosleep(200);
+  for (int spins = 0; is_unfilled(x); ++spins) {
+    __nanosleep(spins < 64 ? 100 : 1000);
     x = __ldcg(src);
+    if ((spins & 63) == 63) {
+      if (*reinterpret_cast<volatile unsigned long long*>(sync_error) != 0ull) break;
+      if (limit_ns != 0ull && global_ns() - t0 > limit_ns) {
+        atomicOr(sync_error, 1ull);
+        break;
+      }
+    }
   }
-  if (is_unfilled(x)) atomicOr(sync_error, 1ull);
   return x;
 }
 
@@ -1175,7 +1196,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           if (!filled) {
 #pragma unroll 1
             for (int v = 0; v < 5; ++v) {
-              const Real x = wait_filled(slot + v * N2, P.sync_error);
+              const Real x = wait_filled(slot + v * N2, P.sync_error, P.wait_limit_ns);
               pull[0] = v == 0 ? x : pull[0];
               pull[1] = v == 1 ? x : pull[1];
               pull[2] = v == 2 ? x : pull[2];

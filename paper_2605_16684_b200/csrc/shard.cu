@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -163,6 +164,10 @@ public:
       return ESDG_B200_CUDA;
     }
     CU(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    // how long a pull may poll for a pushed lift term before the launch is
+    // declared stuck (rhs_kernel, wait_filled); 0 = no limit (under a debugger)
+    if (const char* ms = std::getenv("ESDG_B200_WAIT_LIMIT_MS"))
+      wait_limit_ns_ = 1000000ull * std::strtoull(ms, nullptr, 10);
     sm_count_ = prop.multiProcessorCount;
     smem_per_sm_ = prop.sharedMemPerMultiprocessor;
 
@@ -579,6 +584,7 @@ private:
     P.face_roles = share ? (groups ? roles_split_ : roles_all_) : nullptr;
     P.frec = frec_;
     P.sync_error = flag_ + 1;
+    P.wait_limit_ns = wait_limit_ns_;
     if (mode == kModeVolume && variant_ < 4 && !groups && n_groups == 0) {
       // a rung of the reference's ladder below "symmetric" (kernels.hpp:20-34)
       const int rung = variant_ <= 1 ? dev::kRungRecompute
@@ -706,6 +712,7 @@ private:
   uint8_t *roles_all_ = nullptr, *roles_split_ = nullptr;
   Real* frec_ = nullptr;
   int share_faces_ = 1;
+  unsigned long long wait_limit_ns_ = 2000000000ull;
   int variant_ = 5; // KernelVariant::Balanced
   int epb_ = 1;
   unsigned long long *flag_ = nullptr, *flag_host_ = nullptr;
