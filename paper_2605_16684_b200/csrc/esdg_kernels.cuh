@@ -851,8 +851,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // a_new * (contributions) and `out` is never read.
   const Real* qe = P.q + eg * (5 * N3) + l;
   const Real* pe = P.phi + eg * N3 + l;
-  Real qv[NQ][5], ph[NQ], ltab[kLogTabRegs];
-  static_assert(EPB * N2 * kLogTabRegs >= LogTab<Real>::kReals, "CTA too small for the table");
+  Real qv[NQ][5], ph[NQ];
   {
     // One thread moves the CTA's slabs of q, phi and (accumulate form, odd
     // NQ) out with TMA bulk copies; everybody else only waits on the
@@ -867,7 +866,10 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
       const unsigned bo = (kBulk && read_out)
                               ? (off_o + nel * 5 * N3 * unsigned(sizeof(Real)) + 15u) & ~15u
                               : 0u;
-      mbar_expect_tx(mbar, bq + bp + bo);
+      // the logarithm's table (FP64) comes the same way
+      constexpr unsigned bt = unsigned(LogTab<Real>::kReals * sizeof(Real));
+      mbar_expect_tx(mbar, bq + bp + bo + bt);
+      if (bt) bulk_g2s(logtab, log_table_address(Real(0)), bt, mbar);
       bulk_g2s(smem_raw, reinterpret_cast<const char*>(P.q + slab0) - off_q, bq, mbar);
       bulk_g2s(smem_raw + Map::kStagePhi, reinterpret_cast<const char*>(P.phi + e0 * N3) - off_p, bp,
                mbar);
@@ -875,7 +877,6 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         bulk_g2s(smem_raw + Map::kTend, reinterpret_cast<const char*>(P.out + slab0) - off_o, bo,
                  mbar);
     }
-    load_log_table(ltab, tid, EPB * N2);
     if (active) {
       if (!kBulk && read_out) {
         // padded slab (even NQ): element-wise asynchronous copies
@@ -917,9 +918,6 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
                    : "memory");
     }
   }
-  // the logarithm's table (FP64): fetched behind the state loads, visible to
-  // the CTA before the first logarithm
-  store_log_table(logtab, ltab, tid, EPB * N2);
   {
     // the slabs have landed: every thread takes the raw values of its z line
     // out of the staging area, which the node values are about to overwrite
