@@ -13,22 +13,27 @@
 // Execution model of rhs_kernel (B200: 148 SMs, 64 FP64 lanes/SM, 227 KB smem)
 //   - one CTA owns EPB consecutive (Morton) elements; EPB*NQ^2 threads; thread
 //     (e, l) is "line l of element e" throughout.
-//   - phase A: every global load is issued first -- the NQ nodes of the
-//     thread's z line (coalesced over l), the logarithm table, L2 prefetches
-//     for the next resident wave and, in the accumulate form, cp.async copies
-//     of the old `out` into the shared tendency slab. Then primitives and both
+//   - phase A: one thread moves the CTA's contiguous slabs of q, phi, the old
+//     `out` (accumulate form) and the logarithm table with TMA bulk copies
+//     and prefetches the next resident wave's slabs into L2. Then primitives and both
 //     logarithms once per node (precompute/logmean rungs of the reference's
 //     ladder), the NQ nodes stage by stage, parked in shared memory, SoA per
 //     quantity.
 //   - the slab holds T = out_old + gain * (contributions), gain = a_new/a_old;
 //     every later phase adds its share with one FMA, the commit writes
 //     a_old * T (a_old == 0: a_new * contributions, `out` is never read).
-//   - phase C (SURF), thread per face node, runs before the sweeps: each
-//     element side evaluates the canonical (minus,plus) flux of its own face
-//     -- the flux is a pure function of the two traces, so both sides obtain
-//     bitwise identical values and conservation is exact without storing
-//     face records. All six faces update the slab; a reflecting wall is the
-//     element's own trace with the normal momentum negated.
+//   - phase C (SURF), thread per face node, runs before the sweeps. The flux
+//     is a pure function of the two traces, and swapping its arguments gives
+//     bitwise the same symmetric part and the negated gravity / dissipation
+//     part, so no face records (17 Reals per face node in the reference) are
+//     stored. K2 and the tiles without dev::Share: each element side evaluates
+//     all six of its faces. One-pass kernels with dev::Share: every interior
+//     face is evaluated once, by the element whose + face it is, which pushes
+//     the other element's lift term (bitwise what that element would compute)
+//     into RhsParams::frec; the other element pulls it -- one TMA bulk copy
+//     per direction, issued before the pair fluxes of that direction -- and
+//     adds it to its line sums. A reflecting wall is the element's own trace
+//     with the normal momentum negated.
 //   - phase B (VOL), thread per node LINE: the thread pulls its line's NQ
 //     nodes into registers and evaluates every unordered pair (i,j) exactly
 //     once, adding c_ij (S + G e_n) to node i and c_ji (S - G b_i/b_j e_n) to
