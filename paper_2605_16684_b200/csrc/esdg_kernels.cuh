@@ -861,7 +861,10 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     // One thread moves the CTA's slabs of q, phi and (accumulate form, odd
     // NQ) out with TMA bulk copies; everybody else only waits on the
     // mbarrier.
-    if (tid == 0) mbar_init(mbar, 1);
+    if (tid == 0) {
+      mbar_init(mbar, 1);
+      if (kBulk) mbar_init(mbar + 1, 1); // the old `out`: not needed before phase C
+    }
     __syncthreads();
     if (tid == 0) {
       const long long left = P.ne - e0;
@@ -873,14 +876,15 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
                               : 0u;
       // the logarithm's table (FP64) comes the same way
       constexpr unsigned bt = unsigned(LogTab<Real>::kReals * sizeof(Real));
-      mbar_expect_tx(mbar, bq + bp + bo + bt);
+      mbar_expect_tx(mbar, bq + bp + bt);
+      if (bo) mbar_expect_tx(mbar + 1, bo);
       if (bt) bulk_g2s(logtab, log_table_address(Real(0)), bt, mbar);
       bulk_g2s(smem_raw, reinterpret_cast<const char*>(P.q + slab0) - off_q, bq, mbar);
       bulk_g2s(smem_raw + Map::kStagePhi, reinterpret_cast<const char*>(P.phi + e0 * N3) - off_p, bp,
                mbar);
       if (kBulk && read_out)
         bulk_g2s(smem_raw + Map::kTend, reinterpret_cast<const char*>(P.out + slab0) - off_o, bo,
-                 mbar);
+                 mbar + 1);
     }
     if (active) {
       if (!kBulk && read_out) {
@@ -1024,6 +1028,8 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   }
   ESDG_CLK();
 
+  // the old `out` has had phase A to arrive in the slab
+  if (kBulk && read_out) mbar_wait(mbar + 1, 0);
   // ---- phase C: the six faces, thread per face node -----------------------
   // Every face subtracts its lift term from the shared tendency slab (zeroed
   // by the z-line owners in phase A). Faces of one direction share no node,
