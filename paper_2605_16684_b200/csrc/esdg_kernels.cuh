@@ -307,6 +307,27 @@ template <> struct Tile<6, 4> : TilePick<ESDG_TUNE_T64E, ESDG_TUNE_T64M> { stati
 template <> struct Tile<7, 4> : TilePick<ESDG_TUNE_T74E, ESDG_TUNE_T74M> { static constexpr int FPI = 1; static constexpr bool LEAN = false; };
 template <> struct Tile<8, 4> : TilePick<ESDG_TUNE_T84E, ESDG_TUNE_T84M> { static constexpr int FPI = 2; static constexpr bool LEAN = false; };
 
+// Which y line a thread of the N = 4 FP64 tile sweeps: entry tid = e * 25 + x +
+// 5 z of the line (element of the CTA, x, z). With the natural assignment
+// (x, z) = (l0, l1) the y lines of a half-warp start 1 and 25 doubles apart and
+// hit the same banks twice: 16 instead of 8 wavefronts per CTA-wide 64-bit
+// access, 31 instead of 16 per 128-bit one. A thread may sweep any y line of
+// its CTA -- the sums go through the slab anyway -- and this permutation
+// (found by local search, tools/yperm_search.py) makes the node loads
+// conflict-free and leaves 11 instead of 16 wavefronts on the slab.
+#ifndef ESDG_TUNE_NO_YPERM
+__constant__ unsigned char c_yperm_5x5[125] = {
+    34, 14, 41, 56, 36, 101, 79, 31, 39, 62, 118, 76, 61, 44, 81, 19, 69, 83, 12, 94, 35, 108, 21, 82, 124,
+    111, 73, 112, 114, 15, 17, 54, 78, 96, 9, 45, 104, 63, 30, 91, 20, 80, 46, 93, 106, 75, 51, 85, 100, 27,
+    58, 68, 5, 105, 47, 38, 26, 67, 123, 8, 13, 64, 6, 117, 48, 113, 59, 53, 22, 24, 55, 74, 71, 60, 109,
+    49, 95, 86, 116, 18, 37, 122, 7, 66, 28, 65, 23, 84, 25, 16, 115, 120, 121, 70, 3, 10, 77, 57, 99, 43,
+    72, 52, 102, 42, 32, 103, 2, 97, 119, 98, 1, 92, 50, 89, 29, 87, 107, 4, 40, 110, 11, 88, 0, 33, 90};
+template <int NQ, int BYTES, int EPB> struct YPerm { static constexpr bool value = NQ == 5 && BYTES == 8 && EPB == 5; };
+#else
+__constant__ unsigned char c_yperm_5x5[1] = {0};
+template <int NQ, int BYTES, int EPB> struct YPerm { static constexpr bool value = false; };
+#endif
+
 // Shared-memory layout of the nine node quantities: three arrays of PAIRS --
 // (rho/2, b), (log rho/2, log b), (phi/2, 1/(2b)) -- followed by the three
 // velocity arrays. A node is then six shared-memory instructions instead of
@@ -800,6 +821,16 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   const int l0 = l % NQ, l1 = l / NQ;
   const long long eg = e0 + e;
   const bool active = eg < P.ne; // only the last CTA has idle lines
+  // the y line this thread sweeps: its own element's (x, z) = (l0, l1), or any
+  // line of the CTA where a bank-conflict-free assignment exists (YPerm)
+  int ey = e, ly0 = l0, ly1 = l1;
+  if (YPerm<NQ, sizeof(Real), EPB>::value) {
+    const int id = c_yperm_5x5[tid];
+    ey = id / N2;
+    const int r = id - ey * N2;
+    ly0 = r % NQ;
+    ly1 = r / NQ;
+  }
   const int zbase = e * N3P + l0 + PX * l1;
   const bool read_out = !VOL || P.a_old != Real(0);
   // The tendency slab as this thread addresses it: variable v of shared index
@@ -811,8 +842,9 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   const unsigned off_p = unsigned(reinterpret_cast<unsigned long long>(P.phi + e0 * N3) & 15u);
   const unsigned off_o = unsigned(reinterpret_cast<unsigned long long>(P.out + slab0) & 15u);
   constexpr int TV = kBulk ? N3P : VS;
-  Real* tslab = kBulk ? reinterpret_cast<Real*>(smem_raw + Map::kTend + off_o) + 4 * e * N3P
-                      : reinterpret_cast<Real*>(smem_raw + Map::kTend);
+  Real* const tslab_own = kBulk ? reinterpret_cast<Real*>(smem_raw + Map::kTend + off_o) + 4 * e * N3P
+                                : reinterpret_cast<Real*>(smem_raw + Map::kTend);
+  Real* const tslab = tslab_own;
 
   // pitches of the three axes in shared (padded) and global node numbering
   auto spitch = [](int ax) { return ax == 0 ? 1 : (ax == 1 ? PX : PX * NQ); };
@@ -1167,9 +1199,13 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         mbar_expect_tx(mbar, bytes);
         bulk_g2s(pbuf, P.frec + (dir * P.ne + e0) * FB, bytes, mbar);
       }
-      if (active) {
+      // the line of this direction: element, and the slab as addressed for it
+      constexpr bool kYPerm = YPerm<NQ, sizeof(Real), EPB>::value;
+      const int ed = (kYPerm && dir == 1) ? ey : e;
+      Real* const tslab = (kYPerm && kBulk && dir == 1) ? tslab_own + 4 * (ey - e) * N3P : tslab_own;
+      if (kYPerm ? (e0 + ed < P.ne) : active) {
         const int base = dir == 0 ? e * N3P + PX * l
-                                  : (dir == 1 ? e * N3P + l0 + ZS * l1 : zbase);
+                                  : (dir == 1 ? ed * N3P + ly0 + ZS * ly1 : zbase);
         const int stride = dir == 0 ? 1 : (dir == 1 ? PX : ZS);
 #pragma unroll
         for (int i = 0; i < NQ; ++i)
@@ -1193,13 +1229,13 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         if (kShare) {
           // The thread that sweeps a line is the face node (s, t) of the
           // line's two faces: (l0, l1), for y lines (l1, l0).
-          const int fn = dir == 1 ? l1 + NQ * l0 : l;
-          Real* slot = P.frec + (dir * P.ne + eg) * FB + fn;
+          const int fn = dir == 1 ? ly1 + NQ * ly0 : l;
+          Real* slot = P.frec + (dir * P.ne + e0 + ed) * FB + fn;
           mbar_wait(mbar, (dir + 1) & 1);
           bool filled = true;
 #pragma unroll
           for (int v = 0; v < 5; ++v) {
-            pull[v] = pbuf[e * FB + v * N2 + fn];
+            pull[v] = pbuf[ed * FB + v * N2 + fn];
             filled = filled && !is_unfilled(pull[v]);
           }
           if (!filled) {
