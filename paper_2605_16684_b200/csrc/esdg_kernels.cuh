@@ -307,25 +307,23 @@ template <> struct Tile<6, 4> : TilePick<ESDG_TUNE_T64E, ESDG_TUNE_T64M> { stati
 template <> struct Tile<7, 4> : TilePick<ESDG_TUNE_T74E, ESDG_TUNE_T74M> { static constexpr int FPI = 1; static constexpr bool LEAN = false; };
 template <> struct Tile<8, 4> : TilePick<ESDG_TUNE_T84E, ESDG_TUNE_T84M> { static constexpr int FPI = 2; static constexpr bool LEAN = false; };
 
-// Which y line a thread of the N = 4 FP64 tile sweeps: entry tid = e * 25 + x +
-// 5 z of the line (element of the CTA, x, z). With the natural assignment
-// (x, z) = (l0, l1) the y lines of a half-warp start 1 and 25 doubles apart and
-// hit the same banks twice: 16 instead of 8 wavefronts per CTA-wide 64-bit
-// access, 31 instead of 16 per 128-bit one. A thread may sweep any y line of
-// its CTA -- the sums go through the slab anyway -- and this permutation
-// (found by local search, tools/yperm_search.py) makes the node loads
-// conflict-free and leaves 11 instead of 16 wavefronts on the slab.
+// Which y line a thread sweeps: YPerm<NQ, BYTES, EPB>::line(tid) = e * NQ^2 + x +
+// NQ z (element of the CTA, x, z). With the natural assignment (x, z) =
+// (l0, l1) the y lines of a half-warp start 1 and PX*NQ words apart and hit
+// the same banks two to three times (N = 4 FP64: 16 instead of 8 wavefronts
+// per CTA-wide 64-bit access, 31 instead of 16 per 128-bit one). A thread
+// may sweep any y line of its CTA -- the sums go through the slab anyway --
+// and the tables of esdg_yperm_tables.inc (local search,
+// tools/yperm_search.py) remove the conflicts of the node loads and most of
+// the slab's (N = 4 FP64: K1 -2.7 %, stage kernel -0.9 %). The table belongs to
+// one tile shape; any other EPB falls back to the natural assignment.
+template <int NQ, int BYTES, int EPB>
+struct YPerm {
+  static constexpr bool value = false;
+  __device__ static __forceinline__ int line(int tid) { return tid; }
+};
 #ifndef ESDG_TUNE_NO_YPERM
-__constant__ unsigned char c_yperm_5x5[125] = {
-    34, 14, 41, 56, 36, 101, 79, 31, 39, 62, 118, 76, 61, 44, 81, 19, 69, 83, 12, 94, 35, 108, 21, 82, 124,
-    111, 73, 112, 114, 15, 17, 54, 78, 96, 9, 45, 104, 63, 30, 91, 20, 80, 46, 93, 106, 75, 51, 85, 100, 27,
-    58, 68, 5, 105, 47, 38, 26, 67, 123, 8, 13, 64, 6, 117, 48, 113, 59, 53, 22, 24, 55, 74, 71, 60, 109,
-    49, 95, 86, 116, 18, 37, 122, 7, 66, 28, 65, 23, 84, 25, 16, 115, 120, 121, 70, 3, 10, 77, 57, 99, 43,
-    72, 52, 102, 42, 32, 103, 2, 97, 119, 98, 1, 92, 50, 89, 29, 87, 107, 4, 40, 110, 11, 88, 0, 33, 90};
-template <int NQ, int BYTES, int EPB> struct YPerm { static constexpr bool value = NQ == 5 && BYTES == 8 && EPB == 5; };
-#else
-__constant__ unsigned char c_yperm_5x5[1] = {0};
-template <int NQ, int BYTES, int EPB> struct YPerm { static constexpr bool value = false; };
+#include "esdg_yperm_tables.inc"
 #endif
 
 // Shared-memory layout of the nine node quantities: three arrays of PAIRS --
@@ -823,9 +821,12 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   const bool active = eg < P.ne; // only the last CTA has idle lines
   // the y line this thread sweeps: its own element's (x, z) = (l0, l1), or any
   // line of the CTA where a bank-conflict-free assignment exists (YPerm)
+  // (not in the one-pass kernels of N = 6: the extra registers spill there and
+  // cost more than the conflicts, +1.3 %)
+  constexpr bool kYPerm = YPerm<NQ, sizeof(Real), EPB>::value && !(SURF && NQ == 7);
   int ey = e, ly0 = l0, ly1 = l1;
-  if (YPerm<NQ, sizeof(Real), EPB>::value) {
-    const int id = c_yperm_5x5[tid];
+  if (kYPerm) {
+    const int id = YPerm<NQ, sizeof(Real), EPB>::line(tid);
     ey = id / N2;
     const int r = id - ey * N2;
     ly0 = r % NQ;
@@ -1200,7 +1201,6 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         bulk_g2s(pbuf, P.frec + (dir * P.ne + e0) * FB, bytes, mbar);
       }
       // the line of this direction: element, and the slab as addressed for it
-      constexpr bool kYPerm = YPerm<NQ, sizeof(Real), EPB>::value;
       const int ed = (kYPerm && dir == 1) ? ey : e;
       Real* const tslab = (kYPerm && kBulk && dir == 1) ? tslab_own + 4 * (ey - e) * N3P : tslab_own;
       if (kYPerm ? (e0 + ed < P.ne) : active) {

@@ -51,3 +51,17 @@ def test_work_models_agree():
             assert (b["volume_flops"], b["volume_bytes"]) == r["volume"]
             assert (b["surface_flops"], b["surface_bytes"]) == r["surface"]
             assert b["update_bytes"] == r["update"][1]
+
+
+def test_yperm_tables_are_permutations():
+    """csrc/esdg_yperm_tables.inc (tools/yperm_search.py): every table assigns each y
+    line of its tile to exactly one thread."""
+    import re
+    path = os.path.join(ROOT, "paper_2605_16684_b200", "csrc", "esdg_yperm_tables.inc")
+    text = open(path).read()
+    tables = re.findall(r"c_yperm_(\d+)_(\d+)_(\d+)\[(\d+)\] = \{([^}]*)\}", text)
+    assert len(tables) >= 4
+    for nq, nbytes, epb, n, body in tables:
+        vals = [int(v) for v in body.replace("\n", " ").split(",") if v.strip()]
+        assert len(vals) == int(n) == int(epb) * int(nq) ** 2
+        assert sorted(vals) == list(range(int(n)))
