@@ -201,10 +201,11 @@ def test_baroclinic_jet_is_balanced(mode):
 
 
 def test_library_is_a_product_build():
-    """The ladder rungs and tuning hooks are compile-time switches (make
-    EXTRA=-DESDG_LADDER_... / -DESDG_TUNE_...); the library the tests, smoke()
-    and bench.py load must not carry any of them. The Makefile records the
-    flags of the last build and rebuilds everything when they change."""
+    """The tuning hooks are compile-time switches (make EXTRA=-DESDG_TUNE_...);
+    the library the tests, smoke() and bench.py load must not carry any of
+    them. (The ladder rungs are run-time selectable instances, not switches.)
+    The Makefile records the flags of the last build and rebuilds everything
+    when they change."""
     flags = open(os.path.join(capi.CSRC, "build", ".flags")).read()
     assert "ESDG_LADDER" not in flags and "ESDG_TUNE" not in flags, flags
     assert "arch=compute_100a,code=sm_100a" in flags and "-lineinfo" in flags
