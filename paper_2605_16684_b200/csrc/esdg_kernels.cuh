@@ -97,6 +97,10 @@ struct RhsParams {
   const uint8_t* face_roles;
   Real* frec;            // [3][element][FrecBlock<Real, NQ>]: slot f = face lf = 2f, [5][NQ^2] + pad
   unsigned long long* sync_error;
+  // launch-order ticket (null: blockIdx.x is the order): CTA number = value of
+  // the counter when the CTA starts, minus ticket_base
+  unsigned* ticket;
+  unsigned ticket_base;
   unsigned long long wait_limit_ns; // bound of a pull's poll (0: none), ESDG_B200_WAIT_LIMIT_MS
   int flat_phi;          // phi is constant along x and y lines (checked by the host)
   int prefetch_ctas;     // resident CTAs chip-wide: L2 prefetch distance
@@ -800,9 +804,25 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   constexpr int FB = FrecBlock<Real, NQ>::value;
 
   const int tid = threadIdx.x;
+  // Position of this CTA in the launch order. Pulling a lift term may wait for
+  // the group that pushes it, and that group must then be running or done: with
+  // a ticket drawn when the CTA starts, every lower number has started by
+  // construction (the hardware's dispatch order of blockIdx.x does the same in
+  // practice, but is not a documented guarantee).
+  // (the ticket rides on the barrier that publishes the mbarriers)
+  unsigned bid = blockIdx.x;
+  {
+    unsigned* slot = reinterpret_cast<unsigned*>(smem_raw + Map::kTend - 16);
+    if (tid == 0) {
+      if (P.ticket) *slot = atomicAdd(P.ticket, 1u) - P.ticket_base;
+      mbar_init(mbar, 1);
+      if (kBulk) mbar_init(mbar + 1, 1); // the old `out`: not needed before phase C
+    }
+    __syncthreads();
+    if (P.ticket) bid = *slot;
+  }
   const long long e0 =
-      static_cast<long long>(P.groups ? P.groups[blockIdx.x]
-                                      : int32_t(blockIdx.x) + P.group_base) * EPB;
+      static_cast<long long>(P.groups ? P.groups[bid] : int32_t(bid) + P.group_base) * EPB;
 #ifdef ESDG_TUNE_PHASE_CLOCKS
   long long tclk[10];
   int nclk = 0;
@@ -895,11 +915,6 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     // NQ) out with TMA bulk copies; everybody else only waits on the
     // mbarrier.
     if (tid == 0) {
-      mbar_init(mbar, 1);
-      if (kBulk) mbar_init(mbar + 1, 1); // the old `out`: not needed before phase C
-    }
-    __syncthreads();
-    if (tid == 0) {
       const long long left = P.ne - e0;
       const unsigned nel = left < EPB ? unsigned(left) : unsigned(EPB);
       const unsigned bq = (off_q + nel * 5 * N3 * unsigned(sizeof(Real)) + 15u) & ~15u;
@@ -945,7 +960,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   {
     long long en = e0 + static_cast<long long>(P.prefetch_ctas) * EPB;
     if (P.groups) {
-      const unsigned nb = blockIdx.x + unsigned(P.prefetch_ctas);
+      const unsigned nb = bid + unsigned(P.prefetch_ctas);
       en = nb < gridDim.x ? static_cast<long long>(P.groups[nb]) * EPB : P.ne;
     }
     if (tid < 3 && en + EPB <= P.ne && (tid < 2 || read_out)) {

@@ -584,6 +584,9 @@ private:
     P.face_roles = share ? (groups ? roles_split_ : roles_all_) : nullptr;
     P.frec = frec_;
     P.sync_error = flag_ + 1;
+    P.ticket = (share && use_ticket_) ? ticket_ : nullptr;
+    P.ticket_base = ticket_base_;
+    if (P.ticket) ticket_base_ += unsigned((groups || n_groups > 0) ? n_groups : (ne_ + epb_ - 1) / epb_);
     P.wait_limit_ns = wait_limit_ns_;
     if (mode == kModeVolume && variant_ < 4 && !groups && n_groups == 0) {
       // a rung of the reference's ladder below "symmetric" (kernels.hpp:20-34)
@@ -638,6 +641,9 @@ private:
         size_t(std::max<int64_t>(ne_, 1)) * 3 * ((sizeof(Real) * 5 * size_t(n2_) + 15) & ~size_t(15)) + 64;
     CU(cudaMalloc(&frec_, frec_bytes));
     CU(cudaMemset(frec_, 0xff, frec_bytes));
+    CU(cudaMalloc(&ticket_, sizeof(unsigned)));
+    CU(cudaMemset(ticket_, 0, sizeof(unsigned)));
+    if (const char* t = std::getenv("ESDG_B200_TICKET")) use_ticket_ = std::atoi(t);
     interior.insert(interior.end(), boundary.begin(), boundary.end());
     CU(alloc_copy(&groups_, interior.data(), sizeof(int32_t) * interior.size()));
     return ESDG_B200_OK;
@@ -678,6 +684,7 @@ private:
     cudaFree(roles_all_);
     cudaFree(roles_split_);
     cudaFree(frec_);
+    cudaFree(ticket_);
     cudaFree(ghost_phi_);
     cudaFree(send_elem_);
     cudaFree(send_face_);
@@ -712,6 +719,9 @@ private:
   uint8_t *roles_all_ = nullptr, *roles_split_ = nullptr;
   Real* frec_ = nullptr;
   int share_faces_ = 1;
+  unsigned* ticket_ = nullptr; // launch-order counter of the one-pass kernels
+  unsigned ticket_base_ = 0;
+  int use_ticket_ = 1;
   unsigned long long wait_limit_ns_ = 2000000000ull;
   int variant_ = 5; // KernelVariant::Balanced
   int epb_ = 1;
