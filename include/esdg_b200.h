@@ -366,6 +366,14 @@ int esdg_b200_solver_create_nccl(esdg_b200_mesh* mesh, int order,
                                  int precision, int world_size, int rank,
                                  int device, const void* id128,
                                  esdg_b200_solver** out);
+/* The exchange routine of the process-per-GPU path (one ncclRecv / ncclSend
+ * pair per peer in one group on a stream, nccl_transport.cpp) run against
+ * ITSELF: a one-rank communicator on `device`, `count` values of `precision`
+ * (4 or 8) bytes sent to and received from rank 0 in one group, in two peer
+ * blocks. *mismatches = values that did not arrive intact. All a one-GPU box
+ * can show of the NCCL data plane. */
+int esdg_b200_nccl_selftest(int device, int precision, int64_t count,
+                            int64_t* mismatches);
 /* NCCL_VERSION_CODE of the library bound by create_nccl (0: none) */
 int esdg_b200_solver_nccl_version(const esdg_b200_solver* s);
 void esdg_b200_solver_destroy(esdg_b200_solver* s);

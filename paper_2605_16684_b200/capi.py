@@ -132,6 +132,7 @@ SIGNATURES = {
     "esdg_b200_solver_destroy": (None, [_vp]),
     "esdg_b200_solver_set_path": (_i, [_vp, _i]),
     "esdg_b200_face_roles": (_i, [_ip, _i64, _i, _i, _vp]),
+    "esdg_b200_nccl_selftest": (_i, [_i, _i, _i64, _i64p]),
     "esdg_b200_solver_set_overlap": (_i, [_vp, _i]),
     "esdg_b200_solver_set_face_sharing": (_i, [_vp, _i]),
     "esdg_b200_solver_overlap_elements": (_i, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),

@@ -220,6 +220,56 @@ int esdg_b200_nccl_unique_id(void* id128) {
   return ESDG_B200_OK;
 }
 
+int esdg_b200_nccl_selftest(int device, int precision, int64_t count, int64_t* mismatches) {
+  if ((precision != 4 && precision != 8) || count < 2 || !mismatches) {
+    esdg_b200::set_message("nccl_selftest: bad argument");
+    return ESDG_B200_BADARG;
+  }
+  *mismatches = -1;
+  std::string why;
+  char id[esdg_b200::host::kNcclUniqueIdBytes];
+  if (cudaSetDevice(device) != cudaSuccess) {
+    esdg_b200::set_message("nccl_selftest: cudaSetDevice failed");
+    return ESDG_B200_CUDA;
+  }
+  esdg_b200::host::NcclTransport t;
+  if (!esdg_b200::host::NcclTransport::unique_id(id, &why) || !t.init(1, 0, id, &why)) {
+    esdg_b200::set_message("nccl_selftest: " + why);
+    return ESDG_B200_CUDA;
+  }
+  const size_t bytes = size_t(count) * size_t(precision);
+  std::vector<unsigned char> h_send(bytes), h_recv(bytes, 0);
+  for (size_t i = 0; i < bytes; ++i) h_send[i] = static_cast<unsigned char>(i * 131u + 7u);
+  void *d_send = nullptr, *d_recv = nullptr;
+  cudaStream_t st = nullptr;
+  bool ok = cudaMalloc(&d_send, bytes) == cudaSuccess && cudaMalloc(&d_recv, bytes) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaMemcpy(d_send, h_send.data(), bytes, cudaMemcpyHostToDevice) == cudaSuccess &&
+            cudaMemset(d_recv, 0, bytes) == cudaSuccess;
+  if (ok) {
+    // two peer blocks, both "peers" being this rank: what a partition with
+    // two neighbours issues per RHS
+    const long long half = count / 2;
+    const long long off[2] = {0, half}, cnt[2] = {half, count - half};
+    const int peer[2] = {0, 0};
+    ok = t.exchange(d_send, d_recv, off, cnt, peer, 2, precision, st, &why) &&
+         cudaStreamSynchronize(st) == cudaSuccess &&
+         cudaMemcpy(h_recv.data(), d_recv, bytes, cudaMemcpyDeviceToHost) == cudaSuccess;
+  }
+  if (st) cudaStreamDestroy(st);
+  cudaFree(d_send);
+  cudaFree(d_recv);
+  if (!ok) {
+    esdg_b200::set_message("nccl_selftest: " + (why.empty() ? std::string("CUDA error") : why));
+    return ESDG_B200_CUDA;
+  }
+  int64_t bad = 0;
+  for (int64_t i = 0; i < count; ++i)
+    if (std::memcmp(&h_send[size_t(i) * precision], &h_recv[size_t(i) * precision], size_t(precision)) != 0) ++bad;
+  *mismatches = bad;
+  return ESDG_B200_OK;
+}
+
 int esdg_b200_solver_create_nccl(esdg_b200_mesh* mesh, int order, const esdg_b200_gas* gas,
                                  const esdg_b200_settings* settings, int precision,
                                  int world_size, int rank, int device, const void* id128,

@@ -161,6 +161,21 @@ def test_partitions_on_several_devices_bitwise(path):
         assert np.array_equal(s.get_state(), one.get_state()), parts
 
 
+@pytest.mark.parametrize("precision", [8, 4])
+def test_nccl_exchange_routine_against_itself(precision):
+    """The C++ exchange routine of the process-per-GPU path (NcclTransport::
+    exchange: one ncclRecv / ncclSend pair per peer block in one group on a
+    stream) on a one-rank communicator, both peer blocks addressed to rank 0:
+    everything of the NCCL data plane a one-GPU box can execute -- run-time
+    binding of libnccl.so.2, communicator, grouped point-to-point on the
+    library's own stream, the byte layout of the blocks."""
+    import ctypes as C
+    bad = C.c_int64(-1)
+    rc = capi.lib().esdg_b200_nccl_selftest(0, precision, 5 * 25 * 1000 + 3, C.byref(bad))
+    assert rc == 0, capi.lib().esdg_b200_last_message().decode()
+    assert bad.value == 0
+
+
 def _nccl_worker(rank, world, path, out_dir):
     torch.cuda.set_device(rank)
     id_file = os.path.join(out_dir, "nccl_id.bin")
