@@ -267,10 +267,13 @@ int esdg_b200_exchange_plan(esdg_b200_mesh* m, int ranks, int32_t* ghost_count,
  * elements_per_group consecutive elements per CTA (esdg_b200_rhs_launch_shape).
  * roles[e]: bit f (0..2) = the lift term of face lf = 2f of e is pushed by the
  * element across it, bit 3+d = e pushes the term of its face lf = 2d+1. split
- * != 0: the table for the interior / boundary list launches (no sharing
- * between a group with and a group without a ghost face). Every interior face
- * keeps exactly one evaluator: the reference's one record per face
- * (compute_face_record, kernels.hpp:350-384). */
+ * != 0: the table for the interior / boundary list launches (the interior
+ * list runs first, so its elements may push to the boundary list's, never the
+ * other way round). A face is shared only if the element that evaluates it
+ * comes no later in the launch order than the one that takes the result; the
+ * others, like walls and ghost faces, are evaluated by both sides -- to
+ * bitwise the same number (the reference keeps one record per face for this,
+ * compute_face_record, kernels.hpp:350-384). */
 int esdg_b200_face_roles(const int32_t* nbr_local, int64_t n_elements,
                          int elements_per_group, int split, uint8_t* roles);
 /* Host-only: the GPU-side slice of the exchange for partition `rank` of

@@ -88,12 +88,12 @@ void build_rank_halo(const Mesh& m, const std::vector<int64_t>& rb, int r,
 // B (its - face, lf - 1) is always evaluated by A; B takes A's result instead
 // of evaluating the face a second time (bit f of roles[B], f = lf / 2; bit
 // 3 + f of roles[A] tells A to push it) when A's group is dispatched no later
-// than B's in the same launch: A < B for a launch over all groups or over
-// consecutive runs of them (split == false), and additionally the same list
-// (group with / without a ghost face) for the interior / boundary launches
-// (split == true). Everything else -- walls, ghost faces, periodic
-// wrap-around (A has the higher index there), faces between the two lists --
-// B evaluates itself.
+// than B's: A < B for a launch over all groups or over consecutive runs of
+// them (split == false); for the interior / boundary launches (split == true)
+// A < B inside a list, and between the lists A in the interior list (which
+// is launched, and has finished, before the boundary list). Everything else
+// -- walls, ghost faces, periodic wrap-around (A has the higher index there),
+// a boundary-list A next to an interior-list B -- B evaluates itself.
 void build_face_roles(const int32_t* nbr, int64_t ne, int epb, bool split, uint8_t* roles);
 
 // Named initial conditions (cases.hpp of the reference + our baroclinic one).

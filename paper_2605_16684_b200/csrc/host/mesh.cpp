@@ -209,8 +209,15 @@ void build_face_roles(const int32_t* nbr, int64_t ne, int epb, bool split, uint8
   for (int64_t b = 0; b < ne; ++b)
     for (int f = 0; f < 3; ++f) {
       const int32_t a = nbr[b * 6 + 2 * f];
-      if (a < 0 || a >= b || nbr[int64_t(a) * 6 + 2 * f + 1] != int32_t(b)) continue;
-      if (split && boundary[size_t(a / epb)] != boundary[size_t(b / epb)]) continue;
+      if (a < 0 || a == b || nbr[int64_t(a) * 6 + 2 * f + 1] != int32_t(b)) continue;
+      if (split) {
+        // the interior list is launched (and finished) before the boundary
+        // list: inside a list the index decides, between the lists the launch
+        const int la = boundary[size_t(a / epb)], lb = boundary[size_t(b / epb)];
+        if (la > lb || (la == lb && a > b)) continue;
+      } else if (a > b) {
+        continue;
+      }
       roles[b] |= uint8_t(1u << f);
       roles[a] |= uint8_t(8u << f);
     }

@@ -52,20 +52,26 @@ def test_every_local_face_has_one_evaluator(name, cfg, epb, world, split):
                 if pulled:
                     # the pusher is a local element across that very face, dispatched no
                     # later than the puller, and it knows that it has to push
-                    assert 0 <= a < b
+                    assert a >= 0 and a != b
                     assert int(nbr[a, 2 * f + 1]) == b
                     assert roles[a] >> (3 + f) & 1
                     if split:
-                        assert ghost_group[a // epb] == ghost_group[b // epb]
+                        # launch order: interior list first, then the boundary list
+                        ka, kb = (ghost_group[a // epb], a), (ghost_group[b // epb], b)
+                        assert ka < kb
+                    else:
+                        assert a < b
                 else:
                     # evaluated by b itself: wall, ghost, wrap-around, self-neighbour, other list
-                    ok = a < 0 or a >= b or int(nbr[a, 2 * f + 1]) != b or \
-                        (split and ghost_group[a // epb] != ghost_group[b // epb])
-                    assert ok, (b, f, a)
+                    if split and a >= 0:
+                        later = (ghost_group[a // epb], a) >= (ghost_group[b // epb], b)
+                    else:
+                        later = a >= b
+                    assert a < 0 or later or int(nbr[a, 2 * f + 1]) != b, (b, f, a)
             for d in range(3):
                 if roles[b] >> (3 + d) & 1:
                     a = int(nbr[b, 2 * d + 1])
-                    assert a > b and roles[a] >> d & 1 and int(nbr[a, 2 * d]) == b
+                    assert a != b and roles[a] >> d & 1 and int(nbr[a, 2 * d]) == b
         # pushes and pulls pair up one to one
         assert sum(bin(int(r) & 7).count("1") for r in roles) == sum(bin(int(r) >> 3).count("1") for r in roles)
 
