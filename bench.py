@@ -310,8 +310,11 @@ def main_b200(args, rank, local_rank, world):
                                 distributed=(world, rank, device))
         cb, exchange = halo.make_exchange_callback(solver, device)
         solver.exchange_impl = cb
-    else:
+    elif world == 1:
         solver = capi.GpuSolver(mesh, args.order, args.precision, settings=settings, devices=[device])
+    assert solver is not None
+    if world > 1 and solver.end - solver.begin >= mesh.ne:
+        raise RuntimeError(f"rank {rank} of {world} holds the whole mesh: the partitioned solver was not created")
     solver.set_path({"stage": capi.PATH_STAGE, "fused": capi.PATH_FUSED, "split": capi.PATH_SPLIT}[args.path])
     solver.init_case(case_id)
     dt_local = solver.compute_dt(0.5)

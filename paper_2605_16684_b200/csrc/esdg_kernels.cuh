@@ -306,7 +306,11 @@ template <> struct Tile<8, 8> { static constexpr int EPB = 1, MINB = 3; static c
 template <> struct Tile<2, 4> { static constexpr int EPB = 32, MINB = 4; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
 template <> struct Tile<3, 4> { static constexpr int EPB = 14, MINB = 4; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
 template <> struct Tile<4, 4> { static constexpr int EPB = 8, MINB = 4; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
-template <> struct Tile<5, 4> { static constexpr int EPB = 5, MINB = 5; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
+#ifndef ESDG_TUNE_T54E
+#define ESDG_TUNE_T54E 5
+#define ESDG_TUNE_T54M 5
+#endif
+template <> struct Tile<5, 4> { static constexpr int EPB = ESDG_TUNE_T54E, MINB = ESDG_TUNE_T54M; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
 template <> struct Tile<6, 4> : TilePick<ESDG_TUNE_T64E, ESDG_TUNE_T64M> { static constexpr int FPI = 1; static constexpr bool LEAN = false; };
 template <> struct Tile<7, 4> : TilePick<ESDG_TUNE_T74E, ESDG_TUNE_T74M> { static constexpr int FPI = 1; static constexpr bool LEAN = false; };
 template <> struct Tile<8, 4> : TilePick<ESDG_TUNE_T84E, ESDG_TUNE_T84M> { static constexpr int FPI = 2; static constexpr bool LEAN = false; };
