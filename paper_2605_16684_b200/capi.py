@@ -15,7 +15,8 @@ import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
-LIB_PATH = os.path.join(CSRC, "libesdg_b200.so")
+# (development: ESDG_B200_LIB points tools/ab_probe.sh at another build of the same library)
+LIB_PATH = os.environ.get("ESDG_B200_LIB") or os.path.join(CSRC, "libesdg_b200.so")
 
 OK, NONPHYSICAL, CUDA, BADARG = 0, 1, 2, 3
 REG_Q, REG_K = 0, 1

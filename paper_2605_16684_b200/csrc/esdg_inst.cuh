@@ -1,5 +1,6 @@
 // esdg_inst.cuh -- body shared by inst_nq*.cu; define ESDG_NQ before including.
 #include <atomic>
+#include <type_traits>
 
 #include "esdg_kernels.cuh"
 #include "esdg_launch.hpp"
@@ -11,8 +12,12 @@ constexpr int kMaxDevices = 64;
 template <class Real, int NQ, bool VOL, bool SURF, int RUNG = dev::kRungProduct>
 cudaError_t launch_one(const dev::RhsParams<Real, NQ>& P, long long n_groups,
                        cudaStream_t stream) {
-  constexpr int EPB = dev::Tile<NQ, sizeof(Real)>::EPB;
-  constexpr int MINB = dev::Tile<NQ, sizeof(Real)>::MINB;
+  // the one-pass kernels (group lists, shared faces) and the split kernels may
+  // use different tiles (dev::TileSplit)
+  using TileT = std::conditional_t<VOL && SURF, dev::Tile<NQ, sizeof(Real)>,
+                                   dev::TileSplit<NQ, sizeof(Real)>>;
+  constexpr int EPB = TileT::EPB;
+  constexpr int MINB = TileT::MINB;
   constexpr int T = EPB * NQ * NQ;
 #ifndef ESDG_TUNE_EXTRA_SMEM
 #define ESDG_TUNE_EXTRA_SMEM 0
@@ -79,11 +84,13 @@ cudaError_t launch_pack(const Real* q, const int32_t* send_elem,
 }
 
 template <class Real, int NQ>
-void rhs_launch_shape(int* threads, int* epb, size_t* smem_bytes) {
-  constexpr int EPB = dev::Tile<NQ, sizeof(Real)>::EPB;
-  *threads = EPB * NQ * NQ;
-  *epb = EPB;
-  *smem_bytes = dev::SmemMap<Real, NQ, EPB>::kBytes;
+void rhs_launch_shape(int mode, int* threads, int* epb, size_t* smem_bytes) {
+  constexpr int E1 = dev::Tile<NQ, sizeof(Real)>::EPB;
+  constexpr int E2 = dev::TileSplit<NQ, sizeof(Real)>::EPB;
+  const bool one_pass = mode == kModeFused;
+  *threads = (one_pass ? E1 : E2) * NQ * NQ;
+  *epb = one_pass ? E1 : E2;
+  *smem_bytes = one_pass ? dev::SmemMap<Real, NQ, E1>::kBytes : dev::SmemMap<Real, NQ, E2>::kBytes;
 }
 
 #define ESDG_INSTANTIATE(REAL, NQ)                                             \
@@ -92,7 +99,7 @@ void rhs_launch_shape(int* threads, int* epb, size_t* smem_bytes) {
   template cudaError_t launch_pack<REAL, NQ>(const REAL*, const int32_t*,      \
                                              const int32_t*, REAL*, long long, \
                                              cudaStream_t);                    \
-  template void rhs_launch_shape<REAL, NQ>(int*, int*, size_t*);
+  template void rhs_launch_shape<REAL, NQ>(int, int*, int*, size_t*);
 
 #endif // ESDG_INST_LADDER
 

@@ -92,10 +92,13 @@ struct RhsParams {
   // its sums ready. face_roles[e]: bit f (0..2) = the lift term of face
   // lf = 2f of e is pushed by the neighbour, bit 3+d = the term of face
   // lf = 2d+1 is to be pushed to the neighbour. Null: every element evaluates
-  // all six faces. A slot holds an all-ones NaN until it has been filled and
-  // is set back to it by its reader (see rhs_kernel, "pulls").
+  // all six faces. Every value in a slot carries the evaluation it belongs to
+  // in its lowest mantissa bit (`epoch`, alternating; see "tagged lift terms"
+  // below), so a reader tells a fresh term from the previous evaluation's and
+  // nobody has to reset a slot.
   const uint8_t* face_roles;
   Real* frec;            // [3][element][FrecBlock<Real, NQ>]: slot f = face lf = 2f, [5][NQ^2] + pad
+  unsigned epoch;        // 0 / 1: the tag (lowest mantissa bit) of the lift terms of this evaluation
   unsigned long long* sync_error;
   // launch-order ticket (null: blockIdx.x is the order): CTA number = value of
   // the counter when the CTA starts, minus ticket_base
@@ -306,14 +309,30 @@ template <> struct Tile<8, 8> { static constexpr int EPB = 1, MINB = 3; static c
 template <> struct Tile<2, 4> { static constexpr int EPB = 32, MINB = 4; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
 template <> struct Tile<3, 4> { static constexpr int EPB = 14, MINB = 4; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
 template <> struct Tile<4, 4> { static constexpr int EPB = 8, MINB = 4; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
+// FP32 N=4: the one-pass kernels run best as three 10-element CTAs per SM (250
+// threads, 80 registers: stage kernel 4.22 ms against 4.42 ms with five
+// 5-element CTAs -- fewer CTAs in different phases share the instruction
+// cache, which is what bounds the FP32 kernels); the volume-only and
+// surface-only kernels prefer the small tile (2.52 / 2.41 ms against 2.68 /
+// 2.57 ms), see TileSplit.
 #ifndef ESDG_TUNE_T54E
-#define ESDG_TUNE_T54E 5
-#define ESDG_TUNE_T54M 5
+#define ESDG_TUNE_T54E 10
+#define ESDG_TUNE_T54M 3
 #endif
 template <> struct Tile<5, 4> { static constexpr int EPB = ESDG_TUNE_T54E, MINB = ESDG_TUNE_T54M; static constexpr int FPI = 1; static constexpr bool LEAN = false; };
 template <> struct Tile<6, 4> : TilePick<ESDG_TUNE_T64E, ESDG_TUNE_T64M> { static constexpr int FPI = 1; static constexpr bool LEAN = false; };
 template <> struct Tile<7, 4> : TilePick<ESDG_TUNE_T74E, ESDG_TUNE_T74M> { static constexpr int FPI = 1; static constexpr bool LEAN = false; };
 template <> struct Tile<8, 4> : TilePick<ESDG_TUNE_T84E, ESDG_TUNE_T84M> { static constexpr int FPI = 2; static constexpr bool LEAN = false; };
+
+// Launch shape of the volume-only and surface-only kernels (K1, K2, the ladder
+// rungs) where it differs from the one-pass kernels'. Those kernels never see
+// a group list, so their EPB is theirs alone; FPI / LEAN stay Tile's.
+template <int NQ, int BYTES> struct TileSplit : Tile<NQ, BYTES> {};
+#ifndef ESDG_TUNE_S54E
+#define ESDG_TUNE_S54E 5
+#define ESDG_TUNE_S54M 5
+#endif
+template <> struct TileSplit<5, 4> : Tile<5, 4> { static constexpr int EPB = ESDG_TUNE_S54E, MINB = ESDG_TUNE_S54M; };
 
 // Which y line a thread sweeps: YPerm<NQ, BYTES, EPB>::line(tid) = e * NQ^2 + x +
 // NQ z (element of the CTA, x, z). With the natural assignment (x, z) =
@@ -744,13 +763,36 @@ template <class Real, int NQ>
 struct FrecBlock {
   static constexpr int value = int(((5 * NQ * NQ * sizeof(Real) + 15) & ~size_t(15)) / sizeof(Real));
 };
-// "Not filled yet": all ones, a NaN no arithmetic produces.
-__device__ __forceinline__ bool is_unfilled(double x) { return __double_as_longlong(x) == -1ll; }
-__device__ __forceinline__ bool is_unfilled(float x) { return __float_as_int(x) == -1; }
-__device__ __forceinline__ void set_unfilled(double* p) {
-  *reinterpret_cast<long long*>(p) = -1ll;
+// Tagged lift terms. A lift term travels through its slot of frec with the
+// lowest bit of its mantissa replaced by the parity of the evaluation (RHS
+// call) it belongs to; the reader checks the bit and clears it. Every slot is
+// written exactly once per evaluation (by the element across the face or by
+// its own element) before it is read, so "bit == this evaluation's parity"
+// means "filled", the slot needs no reset (15 global stores per thread and
+// 2.65 GB of writes per launch at configs[1] with the earlier NaN marker), and
+// an 8-byte (4-byte) store being atomic, a value is either the previous
+// evaluation's or the new one. Clearing the bit truncates the term by at most
+// one ulp (1.1e-16 / 6e-8 relative, far inside the stated tolerances); the
+// evaluating side clears the same bit of its own term (trunc_tag), so the two
+// sides of a face still subtract exactly opposite mass fluxes, and a term is
+// the same number whether it was pushed or self-evaluated: results stay
+// bitwise independent of the partition count and of face sharing on / off.
+// The host keeps the parity consistent (Shard::open_epoch, shard.cu); slots
+// start as all ones (parity 1).
+__device__ __forceinline__ double tag_term(double x, unsigned bit) {
+  return __hiloint2double(__double2hiint(x), (__double2loint(x) & ~1) | int(bit));
 }
-__device__ __forceinline__ void set_unfilled(float* p) { *reinterpret_cast<int*>(p) = -1; }
+__device__ __forceinline__ float tag_term(float x, unsigned bit) {
+  return __int_as_float((__float_as_int(x) & ~1) | int(bit));
+}
+__device__ __forceinline__ bool has_tag(double x, unsigned bit) {
+  return (unsigned(__double2loint(x)) & 1u) == bit;
+}
+__device__ __forceinline__ bool has_tag(float x, unsigned bit) {
+  return (unsigned(__float_as_int(x)) & 1u) == bit;
+}
+__device__ __forceinline__ double trunc_tag(double x) { return tag_term(x, 0u); }
+__device__ __forceinline__ float trunc_tag(float x) { return tag_term(x, 0u); }
 // A lift term that has not arrived although the element evaluating it was
 // dispatched before this one: poll L2 until it is there. The element that
 // pushes never waits for anybody, so this ends. The wait is bounded all the
@@ -767,13 +809,14 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 template <class Real>
-__device__ __noinline__ Real wait_filled(const Real* src, unsigned long long* sync_error,
+__device__ __noinline__ Real wait_filled(const Real* src, unsigned epoch,
+                                        unsigned long long* sync_error,
                                         unsigned long long limit_ns) {
   Real x = __ldcg(src);
-  if (!is_unfilled(x)) return x;
+  if (has_tag(x, epoch)) return x;
   const unsigned long long t0 = global_ns();
 #pragma unroll 1
-  for (int spins = 0; is_unfilled(x); ++spins) {
+  for (int spins = 0; !has_tag(x, epoch); ++spins) {
     __nanosleep(spins < 64 ? 100 : 1000);
     x = __ldcg(src);
     if ((spins & 63) == 63) {
@@ -1067,7 +1110,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           const Real lift = P.lift[dir];
           Real* rec = P.frec + (f * P.ne + eg) * FB + l;
 #pragma unroll
-          for (int v = 0; v < 5; ++v) rec[v * N2] = lift * fl[v];
+          for (int v = 0; v < 5; ++v) rec[v * N2] = tag_term(lift * fl[v], P.epoch);
         }
       }
       // these slots are read back by a bulk copy (async proxy) one thread issues
@@ -1111,7 +1154,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         if (roles & (8u << dir)) {
           Real* rec = P.frec + (dir * P.ne + code) * FB + l;
 #pragma unroll
-          for (int v = 0; v < 5; ++v) rec[v * N2] = lift * fln[v];
+          for (int v = 0; v < 5; ++v) rec[v * N2] = tag_term(lift * fln[v], P.epoch);
         }
         Real* tn = tslab + (1 + dir) * TV;
         Real* tt1 = tslab + (1 + d1) * TV;
@@ -1123,11 +1166,12 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
         o[2] = tt1[s_own];
         o[3] = tt2[s_own];
         o[4] = t4[s_own];
-        tslab[s_own] = fma_(-P.gain, lift * flo[0], o[0]);
-        tn[s_own] = fma_(-P.gain, lift * flo[1], o[1]);
-        tt1[s_own] = fma_(-P.gain, lift * flo[2], o[2]);
-        tt2[s_own] = fma_(-P.gain, lift * flo[3], o[3]);
-        t4[s_own] = fma_(-P.gain, lift * flo[4], o[4]);
+        // (the same truncation the other side's term goes through in its slot)
+        tslab[s_own] = fma_(-P.gain, trunc_tag(lift * flo[0]), o[0]);
+        tn[s_own] = fma_(-P.gain, trunc_tag(lift * flo[1]), o[1]);
+        tt1[s_own] = fma_(-P.gain, trunc_tag(lift * flo[2]), o[2]);
+        tt2[s_own] = fma_(-P.gain, trunc_tag(lift * flo[3]), o[3]);
+        t4[s_own] = fma_(-P.gain, trunc_tag(lift * flo[4]), o[4]);
       }
       __syncthreads();
     }
@@ -1249,18 +1293,18 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           // The thread that sweeps a line is the face node (s, t) of the
           // line's two faces: (l0, l1), for y lines (l1, l0).
           const int fn = dir == 1 ? ly1 + NQ * ly0 : l;
-          Real* slot = P.frec + (dir * P.ne + e0 + ed) * FB + fn;
           mbar_wait(mbar, (dir + 1) & 1);
           bool filled = true;
 #pragma unroll
           for (int v = 0; v < 5; ++v) {
             pull[v] = pbuf[ed * FB + v * N2 + fn];
-            filled = filled && !is_unfilled(pull[v]);
+            filled = filled && has_tag(pull[v], P.epoch);
           }
           if (!filled) {
+            const Real* slot = P.frec + (dir * P.ne + e0 + ed) * FB + fn;
 #pragma unroll 1
             for (int v = 0; v < 5; ++v) {
-              const Real x = wait_filled(slot + v * N2, P.sync_error, P.wait_limit_ns);
+              const Real x = wait_filled(slot + v * N2, P.epoch, P.sync_error, P.wait_limit_ns);
               pull[0] = v == 0 ? x : pull[0];
               pull[1] = v == 1 ? x : pull[1];
               pull[2] = v == 2 ? x : pull[2];
@@ -1268,9 +1312,8 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
               pull[4] = v == 4 ? x : pull[4];
             }
           }
-          // the slot is empty again for the next evaluation
 #pragma unroll
-          for (int v = 0; v < 5; ++v) set_unfilled(slot + v * N2);
+          for (int v = 0; v < 5; ++v) pull[v] = trunc_tag(pull[v]);
           if (dir == 2) {
 #pragma unroll
             for (int v = 0; v < 5; ++v) pull_z[v] = pull[v];
@@ -1354,7 +1397,11 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
 #pragma unroll
       for (int k = 0; k < NQ; ++k)
 #pragma unroll
+#ifdef ESDG_TUNE_NO_QREAD
+        for (int v = 0; v < 5; ++v) qc[k][v] = Real(k + v);
+#else
         for (int v = 0; v < 5; ++v) qc[k][v] = qe[v * N3 + k * N2];
+#endif
     } else if (source) {
       // coriolis_source (physics.hpp:297-306) only needs the momenta
 #pragma unroll

@@ -36,8 +36,9 @@ template <class Real>
 cudaError_t launch_axpy(Real* q, const Real* k, Real b, long long n,
                         cudaStream_t stream);
 
-// Dynamic shared memory one CTA of rhs_kernel needs (bytes) and its CTA size.
+// Dynamic shared memory one CTA of rhs_kernel needs (bytes), its CTA size and
+// elements per CTA, for the kernel of `mode` (RhsMode).
 template <class Real, int NQ>
-void rhs_launch_shape(int* threads, int* epb, size_t* smem_bytes);
+void rhs_launch_shape(int mode, int* threads, int* epb, size_t* smem_bytes);
 
 } // namespace esdg_b200

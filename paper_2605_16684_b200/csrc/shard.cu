@@ -392,7 +392,14 @@ public:
     CU(cudaSetDevice(device_));
     const int32_t* groups = part == ESDG_B200_PART_ALL ? nullptr : groups_ + (part == ESDG_B200_PART_BOUNDARY ? n_groups_[0] : 0);
     const long long n_groups = part == ESDG_B200_PART_ALL ? range_count_ : n_groups_[part - 1];
-    if (part != ESDG_B200_PART_ALL && n_groups == 0) return ESDG_B200_OK;
+    if (mode == kModeFused) {
+      const int rc = open_epoch(part, pick(st));
+      if (rc != ESDG_B200_OK) return rc;
+    }
+    if (part != ESDG_B200_PART_ALL && n_groups == 0) {
+      if (mode == kModeFused) close_epoch(part);
+      return ESDG_B200_OK;
+    }
     cudaError_t e = cudaErrorInvalidValue;
     switch (nq_) {
 #define ESDG_CASE(NQ)                                                          \
@@ -404,9 +411,64 @@ public:
       ESDG_CASE(7) ESDG_CASE(8)
 #undef ESDG_CASE
     }
-    if (e != cudaSuccess) return cuda_fail(e, "rhs_kernel");
+    if (e != cudaSuccess) {
+      frec_parity_ = -1;
+      epoch_state_ = kEpochClosed;
+      return cuda_fail(e, "rhs_kernel");
+    }
+    if (mode == kModeFused) close_epoch(part);
     if (ne_ > 0) ++launches_;
     return ESDG_B200_OK;
+  }
+
+  // Tagged lift terms (esdg_kernels.cuh): the one-pass kernels of one RHS
+  // evaluation -- a launch over all groups, the interior and the boundary
+  // list, or the consecutive runs of stage_fused_range -- write every slot of
+  // frec once, with the evaluation's parity in the lowest mantissa bit, and
+  // read it expecting that parity. Between evaluations every slot therefore
+  // holds the parity of the last one (frec_parity_), and the next evaluation
+  // takes the other. Any call sequence that breaks the pattern (a boundary
+  // launch without its interior launch, an abandoned series of runs, a failed
+  // launch, a pull that timed out) leaves the parities mixed; the next
+  // evaluation then starts from freshly initialised slots (all ones).
+  enum { kEpochClosed = 0, kEpochInteriorDone = 1, kEpochRunsOpen = 2, kEpochSingle = 3, kEpochOrphan = 4 };
+  int open_epoch(int part, cudaStream_t st) {
+    const bool run = part == ESDG_B200_PART_ALL && range_count_ > 0;
+    if ((part == ESDG_B200_PART_BOUNDARY && epoch_state_ == kEpochInteriorDone) ||
+        (run && range_first_ > 0 && epoch_state_ == kEpochRunsOpen))
+      return ESDG_B200_OK; // the evaluation at hand goes on
+    if (epoch_state_ != kEpochClosed || frec_parity_ < 0) {
+      CU(cudaMemsetAsync(frec_, 0xff, frec_bytes_, st));
+      frec_parity_ = 1;
+      ++frec_resets_;
+    }
+    epoch_ = unsigned(1 - frec_parity_);
+    frec_parity_ = -1; // mixed while the evaluation is under way
+    epoch_state_ = part == ESDG_B200_PART_INTERIOR   ? kEpochInteriorDone
+                   : part == ESDG_B200_PART_BOUNDARY ? kEpochOrphan
+                   : (run && range_first_ == 0)      ? kEpochRunsOpen
+                   : run                             ? kEpochOrphan
+                                                     : kEpochSingle;
+    return ESDG_B200_OK;
+  }
+  void close_epoch(int part) {
+    const int64_t total = (ne_ + epb_ - 1) / epb_;
+    bool complete = false;
+    switch (epoch_state_) {
+      case kEpochSingle: complete = true; break;
+      case kEpochInteriorDone:
+        // the boundary list follows, unless it is empty
+        complete = part == ESDG_B200_PART_BOUNDARY || n_groups_[1] == 0;
+        if (!complete) return;
+        break;
+      case kEpochRunsOpen:
+        complete = range_first_ + range_count_ >= total;
+        if (!complete) return;
+        break;
+      default: break; // orphan: the slots stay mixed
+    }
+    frec_parity_ = complete ? int(epoch_) : -1;
+    epoch_state_ = kEpochClosed;
   }
 
   int axpy(double b, cudaStream_t st) override {
@@ -479,6 +541,8 @@ public:
     if (flag_host_[1] != 0) {
       CU(cudaMemsetAsync(flag_ + 1, 0, sizeof(unsigned long long), s));
       CU(cudaStreamSynchronize(s));
+      frec_parity_ = -1; // the slots are re-initialised before the next evaluation
+      epoch_state_ = kEpochClosed;
       set_message("rhs_kernel: an element group waited in vain for the face contributions of an "
                   "earlier group (launch order violated?)");
       return ESDG_B200_CUDA;
@@ -570,7 +634,7 @@ private:
     {
       int threads = 0, epb = 0;
       size_t smem = 0;
-      rhs_launch_shape<Real, NQ>(&threads, &epb, &smem);
+      rhs_launch_shape<Real, NQ>(mode, &threads, &epb, &smem);
       const int per_sm = std::max(1, std::min(int(smem_per_sm_ / std::max<size_t>(smem, 1)), 2048 / std::max(threads, 1)));
       P.prefetch_ctas = sm_count_ * per_sm;
     }
@@ -583,6 +647,7 @@ private:
     const bool share = mode == kModeFused && share_faces_ && frec_ != nullptr;
     P.face_roles = share ? (groups ? roles_split_ : roles_all_) : nullptr;
     P.frec = frec_;
+    P.epoch = epoch_;
     P.sync_error = flag_ + 1;
     P.ticket = (share && use_ticket_) ? ticket_ : nullptr;
     P.ticket_base = ticket_base_;
@@ -607,7 +672,7 @@ private:
     size_t smem = 0;
     switch (nq_) {
 #define ESDG_CASE(NQ) \
-  case NQ: rhs_launch_shape<Real, NQ>(&threads, &epb, &smem); break;
+  case NQ: rhs_launch_shape<Real, NQ>(kModeFused, &threads, &epb, &smem); break;
       ESDG_CASE(2) ESDG_CASE(3) ESDG_CASE(4) ESDG_CASE(5) ESDG_CASE(6)
       ESDG_CASE(7) ESDG_CASE(8)
 #undef ESDG_CASE
@@ -635,12 +700,15 @@ private:
     CU(alloc_copy(&roles_all_, roles[0].data(), size_t(ne_)));
     CU(alloc_copy(&roles_split_, roles[1].data(), size_t(ne_)));
     // blocks of the pushed lift terms, [3][element][5 n2 Reals padded to 16
-    // bytes] (dev::FrecBlock), all "not filled" (an all-ones NaN); + 64: the
+    // bytes] (dev::FrecBlock), all ones = tagged with parity 1 (open_epoch); + 64: the
     // bulk copy of a group's blocks may be issued for the last, partial group
     const size_t frec_bytes =
         size_t(std::max<int64_t>(ne_, 1)) * 3 * ((sizeof(Real) * 5 * size_t(n2_) + 15) & ~size_t(15)) + 64;
     CU(cudaMalloc(&frec_, frec_bytes));
     CU(cudaMemset(frec_, 0xff, frec_bytes));
+    frec_bytes_ = frec_bytes;
+    frec_parity_ = 1; // all ones
+    epoch_state_ = kEpochClosed;
     CU(cudaMalloc(&ticket_, sizeof(unsigned)));
     CU(cudaMemset(ticket_, 0, sizeof(unsigned)));
     if (const char* t = std::getenv("ESDG_B200_TICKET")) use_ticket_ = std::atoi(t);
@@ -718,6 +786,11 @@ private:
   // shared face evaluation of the one-pass kernels (RhsParams::face_roles)
   uint8_t *roles_all_ = nullptr, *roles_split_ = nullptr;
   Real* frec_ = nullptr;
+  size_t frec_bytes_ = 0;
+  int frec_parity_ = 1;   // tag every slot of frec holds (0 / 1), -1: mixed
+  unsigned epoch_ = 0;    // tag of the evaluation under way / last started
+  int epoch_state_ = 0;   // kEpoch*
+  int64_t frec_resets_ = 0;
   int share_faces_ = 1;
   unsigned* ticket_ = nullptr; // launch-order counter of the one-pass kernels
   unsigned ticket_base_ = 0;

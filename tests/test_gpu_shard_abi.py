@@ -194,3 +194,59 @@ def test_shard_abi_lsrk_steps(setup):
             assert lib.esdg_b200_shard_check(sh.s, None, C.byref(err)) == capi.OK
     assert np.array_equal(gather(shards, capi.REG_Q), ref.get_state())
     assert np.array_equal(gather(shards, capi.REG_K), ref.get_state(capi.REG_K))
+
+
+def test_shard_abi_irregular_launch_sequences(setup):
+    """The lift terms shared between elements carry the parity of the RHS
+    evaluation they belong to (tagged lift terms, esdg_kernels.cuh); the shard
+    keeps the parity consistent across the launches of one evaluation. Launch
+    sequences that break the pattern -- an interior launch never followed by
+    its boundary launch, an interior launch repeated, evaluations of
+    different shapes back to back -- must still give the one-launch result,
+    bitwise, afterwards. (A boundary launch always follows its interior
+    launch: its groups pull terms the interior groups push.)"""
+    lib = capi.lib()
+    mesh, ref, q, shards = setup
+    ref.set_path(capi.PATH_FUSED)
+    ref.set_state(q)
+    ref.rhs(0.0, 1.0)
+    want = ref.get_state(capi.REG_K)
+    for sh in shards:
+        sh.upload(capi.REG_Q, q)
+    exchange(shards)
+
+    def full():
+        for sh in shards:
+            capi.check(lib.esdg_b200_shard_rhs_fused(sh.s, capi.REG_Q, capi.REG_K, 0.0, 1.0, 0, None))
+
+    def part(p):
+        for sh in shards:
+            capi.check(lib.esdg_b200_shard_rhs_fused_part(sh.s, capi.REG_Q, capi.REG_K, 0.0, 1.0, 0, p, None))
+
+    def poison():
+        for sh in shards:
+            capi.check(lib.esdg_b200_shard_upload(sh.s, capi.REG_K, np.full(sh.shape, np.nan).ctypes.data_as(C.c_void_p),
+                                                  0, sh.shape[0]))
+
+    def parts():
+        part(1)
+        part(2)
+
+    # (what came before, the complete evaluation whose result is checked)
+    sequences = [
+        ([full, full], full),                          # alternating parities
+        ([], parts),
+        ([lambda: part(1)], full),                     # abandoned evaluation, then a whole one
+        ([lambda: part(1), lambda: part(1)], parts),
+        ([full, parts, full], parts),
+        ([parts, parts, lambda: part(1)], parts),
+    ]
+    err = capi.Error()
+    for before, final in sequences:
+        for launch in before:
+            launch()
+        poison()
+        final()
+        assert np.array_equal(gather(shards, capi.REG_K), want)
+        for sh in shards:
+            assert lib.esdg_b200_shard_check(sh.s, None, C.byref(err)) == capi.OK
