@@ -262,10 +262,19 @@ def main_b200(args, rank, local_rank, world):
         # the NCCL log lets whoever runs this count ranks and see the transport
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
-    device = local_rank
+    # ESDG_BENCH_DIST_BACKEND=gloo (tests only): the ranks of a one-GPU box share
+    # cuda:0 and torch.distributed runs over gloo on host tensors, so that the
+    # multi-rank flow of this file can be exercised where NCCL refuses two ranks
+    # on one device (tests/test_gpu_bench_ranks.py)
+    backend = os.environ.get("ESDG_BENCH_DIST_BACKEND", "nccl") if world > 1 else None
+    device = local_rank % max(torch.cuda.device_count(), 1) if backend == "gloo" else local_rank
     torch.cuda.set_device(device)
+    if world > 1:
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{device}"))
+    cdev = "cpu" if backend == "gloo" else f"cuda:{device}"   # where collectives' tensors live
 
     nq = args.order + 1
     rb = 8 if args.precision == "f64" else 4
@@ -288,7 +297,7 @@ def main_b200(args, rank, local_rank, world):
     if world > 1 and args.exchange == "nccl":
         # the exchange lives in the library: rank 0 makes the NCCL unique id,
         # torch.distributed (plumbing) hands it round, no Python runs in a step
-        uid = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{device}")
+        uid = torch.zeros(128, dtype=torch.uint8, device=cdev)
         if rank == 0:
             uid.copy_(torch.frombuffer(bytearray(capi.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, 0)
@@ -298,7 +307,7 @@ def main_b200(args, rank, local_rank, world):
                                     nccl=(world, rank, device, bytes(uid.cpu().numpy().tobytes())))
         except Exception as exc:  # noqa: BLE001 -- every rank must take the same way out
             print(f"[bench] rank {rank}: library-side NCCL exchange unavailable ({exc})", file=sys.stderr)
-        ok = torch.tensor([1 if solver is not None else 0], dtype=torch.int32, device=f"cuda:{device}")
+        ok = torch.tensor([1 if solver is not None else 0], dtype=torch.int32, device=cdev)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         if int(ok.item()) == 0:
             # fall back to the torch.distributed callback on all ranks alike
@@ -319,7 +328,7 @@ def main_b200(args, rank, local_rank, world):
     solver.init_case(case_id)
     dt_local = solver.compute_dt(0.5)
     if world > 1:
-        t = torch.tensor([dt_local], dtype=torch.float64, device=f"cuda:{device}")
+        t = torch.tensor([dt_local], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         dt_local = float(t.item())
     dt = dt_local
@@ -379,7 +388,7 @@ def main_b200(args, rank, local_rank, world):
     ms, clocks, timers, launches0 = timed_pass()
     redo = 1 if (rank == 0 and suspicious(clocks)) else 0
     if world > 1:
-        t = torch.tensor([redo], dtype=torch.int32, device=f"cuda:{device}")
+        t = torch.tensor([redo], dtype=torch.int32, device=cdev)
         dist.broadcast(t, 0)
         redo = int(t.item())
     if redo:
@@ -390,7 +399,7 @@ def main_b200(args, rank, local_rank, world):
     if rank == 0:
         sampler.stop()
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{device}")
+        t = torch.tensor([ms], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     n_rhs = 5 * args.steps
@@ -424,7 +433,7 @@ def main_b200(args, rank, local_rank, world):
             barrier()
             wall = time.perf_counter() - t0
             if world > 1:
-                t = torch.tensor([wall], dtype=torch.float64, device=f"cuda:{device}")
+                t = torch.tensor([wall], dtype=torch.float64, device=cdev)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 wall = float(t.item())
             return dof_total * 5 * e2e_steps / wall
