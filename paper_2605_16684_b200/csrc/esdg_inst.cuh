@@ -1,5 +1,4 @@
 // esdg_inst.cuh -- body shared by inst_nq*.cu; define ESDG_NQ before including.
-#include <algorithm>
 #include <atomic>
 #include <type_traits>
 
@@ -39,32 +38,7 @@ cudaError_t launch_one(const dev::RhsParams<Real, NQ>& P, long long n_groups,
   // n_groups > 0 without a list: the run of groups starting at P.group_base
   const long long blocks = (P.groups || n_groups > 0) ? n_groups : (P.ne + EPB - 1) / EPB;
   if (blocks <= 0) return cudaSuccess;
-  dev::RhsParams<Real, NQ> Q = P;
-  Q.n_groups = unsigned(blocks);
-  // Persistent form (TMA slab layout with a volume term, see rhs_kernel): as
-  // many CTAs as are resident at once, each working on group after group. A
-  // kernel whose groups wait for lift terms of earlier groups (face_roles)
-  // needs the launch-order ticket for that -- a CTA that has not started must
-  // not own a group others wait for; without the ticket it keeps one CTA per
-  // group.
-  long long grid = blocks;
-  constexpr bool persistent = dev::SmemMap<Real, NQ, EPB>::kBulk && VOL && RUNG == dev::kRungProduct &&
-                              ESDG_PERSIST;
-  if (persistent && (Q.ticket || !Q.face_roles)) {
-    static std::atomic<int> resident[kMaxDevices];
-    int r = (device >= 0 && device < kMaxDevices) ? resident[device].load(std::memory_order_acquire) : 0;
-    if (r == 0) {
-      int per_sm = 0, sms = 0;
-      err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
-      if (err != cudaSuccess) return err;
-      err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-      if (err != cudaSuccess) return err;
-      r = std::max(1, per_sm * sms);
-      if (device >= 0 && device < kMaxDevices) resident[device].store(r, std::memory_order_release);
-    }
-    grid = std::min<long long>(blocks, r);
-  }
-  kern<<<dim3(unsigned(grid)), dim3(T), smem, stream>>>(Q);
+  kern<<<dim3(unsigned(blocks)), dim3(T), smem, stream>>>(P);
   return cudaGetLastError();
 }
 } // namespace

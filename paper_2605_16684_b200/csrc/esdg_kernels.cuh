@@ -52,10 +52,6 @@
 
 #include <cstdio>
 
-#ifndef ESDG_PERSIST
-#define ESDG_PERSIST 0 // 1: persistent CTAs (measured slower, see rhs_kernel and DESIGN.md section 4)
-#endif
-
 #include "esdg_device.cuh"
 
 namespace esdg_b200 {
@@ -108,7 +104,6 @@ struct RhsParams {
   // the counter when the CTA starts, minus ticket_base
   unsigned* ticket;
   unsigned ticket_base;
-  unsigned n_groups;     // element groups of this launch: persistent CTAs work until their number reaches it
   unsigned long long wait_limit_ns; // bound of a pull's poll (0: none), ESDG_B200_WAIT_LIMIT_MS
   int flat_phi;          // phi is constant along x and y lines (checked by the host)
   int prefetch_ctas;     // resident CTAs chip-wide: L2 prefetch distance
@@ -862,18 +857,9 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // construction (the hardware's dispatch order of blockIdx.x does the same in
   // practice, but is not a documented guarantee).
   // (the ticket rides on the barrier that publishes the mbarriers)
-  // Persistent CTAs (TMA slab layout, kernels with a volume term): the grid is
-  // what is resident at once, a CTA works on group after group, and while it
-  // commits one group the next one's q, phi and logarithm table are already on
-  // their way into the node-value arrays (dead by then) -- the wait for the
-  // slabs, the launch of a CTA, its mbarrier set-up and the L2 prefetch of the
-  // non-persistent form disappear from all groups but a CTA's first. The next
-  // group's number is a fresh ticket (or, without tickets, bid + gridDim.x:
-  // only where no group waits for another, see esdg_inst.cuh).
-  constexpr bool kPersist = kBulk && VOL && RUNG == kRungProduct && ESDG_PERSIST;
-  unsigned* const slot = reinterpret_cast<unsigned*>(smem_raw + Map::kTend - 16);
   unsigned bid = blockIdx.x;
   {
+    unsigned* slot = reinterpret_cast<unsigned*>(smem_raw + Map::kTend - 16);
     if (tid == 0) {
       if (P.ticket) *slot = atomicAdd(P.ticket, 1u) - P.ticket_base;
       mbar_init(mbar, 1);
@@ -882,42 +868,8 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     __syncthreads();
     if (P.ticket) bid = *slot;
   }
-  unsigned ph0 = 0, ph1 = 0; // phase parities of the two mbarriers
-  bool first = true;         // a CTA's first group: nobody has issued its loads yet
-  auto group_start = [&](unsigned b) {
-    return static_cast<long long>(P.groups ? P.groups[b] : int32_t(b) + P.group_base) * EPB;
-  };
-  // thread 0: TMA bulk copies of q, phi and the logarithm table of the group
-  // that starts at element g0, completing on mbar[0]
-  auto issue_loads = [&](long long g0) {
-    const long long left = P.ne - g0;
-    const unsigned nel = left < EPB ? unsigned(left) : unsigned(EPB);
-    const unsigned oq = unsigned(reinterpret_cast<unsigned long long>(P.q + g0 * (5 * N3)) & 15u);
-    const unsigned op = unsigned(reinterpret_cast<unsigned long long>(P.phi + g0 * N3) & 15u);
-    const unsigned bq = (oq + nel * 5 * N3 * unsigned(sizeof(Real)) + 15u) & ~15u;
-    const unsigned bp = (op + nel * N3 * unsigned(sizeof(Real)) + 15u) & ~15u;
-    // the logarithm's table (FP64) comes the same way
-    constexpr unsigned bt = unsigned(LogTab<Real>::kReals * sizeof(Real));
-    mbar_expect_tx(mbar, bq + bp + bt);
-    if (bt) bulk_g2s(logtab, log_table_address(Real(0)), bt, mbar);
-#ifdef ESDG_TUNE_SPLIT_LOADS
-    {
-      // q in ESDG_TUNE_SPLIT_LOADS pieces (16-byte multiples): more bulk copies in flight
-      const char* src = reinterpret_cast<const char*>(P.q + g0 * (5 * N3)) - oq;
-      const unsigned piece = ((bq / ESDG_TUNE_SPLIT_LOADS) + 15u) & ~15u;
-      for (unsigned o = 0; o < bq; o += piece)
-        bulk_g2s(smem_raw + o, src + o, (bq - o) < piece ? (bq - o) : piece, mbar);
-    }
-#else
-    bulk_g2s(smem_raw, reinterpret_cast<const char*>(P.q + g0 * (5 * N3)) - oq, bq, mbar);
-#endif
-    bulk_g2s(smem_raw + Map::kStagePhi, reinterpret_cast<const char*>(P.phi + g0 * N3) - op, bp, mbar);
-  };
-#pragma unroll 1
-  for (;;) {
-  // (a ticket drawn after the last group: nothing left to do)
-  if (bid >= P.n_groups) break;
-  const long long e0 = group_start(bid);
+  const long long e0 =
+      static_cast<long long>(P.groups ? P.groups[bid] : int32_t(bid) + P.group_base) * EPB;
 #ifdef ESDG_TUNE_PHASE_CLOCKS
   long long tclk[10];
   int nclk = 0;
@@ -983,13 +935,6 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // codes were read at kernel start, so a fetch is one round trip, not two.
   constexpr int FPI = Tile<NQ, sizeof(Real)>::FPI;
   NbrRaw<Real> cur[FPI]; // the gathered neighbour trace(s) of the next face iteration
-#pragma unroll
-  for (int f = 0; f < FPI; ++f) {
-#pragma unroll
-    for (int v = 0; v < 5; ++v) cur[f].q[v] = Real(0);
-    cur[f].ph = Real(0);
-    cur[f].code = -1;
-  }
   auto fetch = [&](int lf, NbrRaw<Real>& r) {
     const int dir = lf >> 1, side = lf & 1;
     const int d1 = dir == 2 ? 0 : dir + 1;
@@ -1011,32 +956,30 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // a_new * (contributions) and `out` is never read.
   const Real* qe = P.q + eg * (5 * N3) + l;
   const Real* pe = P.phi + eg * N3 + l;
-  // (defined on every path: a value that is set and used under `active` only
-  // would count as carried from one group of a persistent CTA to the next)
   Real qv[NQ][5], ph[NQ];
-#pragma unroll
-  for (int k = 0; k < NQ; ++k) {
-#pragma unroll
-    for (int v = 0; v < 5; ++v) qv[k][v] = Real(0);
-    ph[k] = Real(0);
-  }
   {
     // One thread moves the CTA's slabs of q, phi and (accumulate form, odd
     // NQ) out with TMA bulk copies; everybody else only waits on the
     // mbarrier.
     if (tid == 0) {
-      // (a persistent CTA's later groups: issued while the previous group was
-      // committed; the slab has been free since that commit's last barrier)
-      if (first) issue_loads(e0);
-      if (kBulk && read_out) {
-        const long long left = P.ne - e0;
-        const unsigned nel = left < EPB ? unsigned(left) : unsigned(EPB);
-        const unsigned bo = (off_o + nel * 5 * N3 * unsigned(sizeof(Real)) + 15u) & ~15u;
-        if (!first) fence_proxy_async_smem();
-        mbar_expect_tx(mbar + 1, bo);
+      const long long left = P.ne - e0;
+      const unsigned nel = left < EPB ? unsigned(left) : unsigned(EPB);
+      const unsigned bq = (off_q + nel * 5 * N3 * unsigned(sizeof(Real)) + 15u) & ~15u;
+      const unsigned bp = (off_p + nel * N3 * unsigned(sizeof(Real)) + 15u) & ~15u;
+      const unsigned bo = (kBulk && read_out)
+                              ? (off_o + nel * 5 * N3 * unsigned(sizeof(Real)) + 15u) & ~15u
+                              : 0u;
+      // the logarithm's table (FP64) comes the same way
+      constexpr unsigned bt = unsigned(LogTab<Real>::kReals * sizeof(Real));
+      mbar_expect_tx(mbar, bq + bp + bt);
+      if (bo) mbar_expect_tx(mbar + 1, bo);
+      if (bt) bulk_g2s(logtab, log_table_address(Real(0)), bt, mbar);
+      bulk_g2s(smem_raw, reinterpret_cast<const char*>(P.q + slab0) - off_q, bq, mbar);
+      bulk_g2s(smem_raw + Map::kStagePhi, reinterpret_cast<const char*>(P.phi + e0 * N3) - off_p, bp,
+               mbar);
+      if (kBulk && read_out)
         bulk_g2s(smem_raw + Map::kTend, reinterpret_cast<const char*>(P.out + slab0) - off_o, bo,
                  mbar + 1);
-      }
     }
     if (active) {
       if (!kBulk && read_out) {
@@ -1062,13 +1005,10 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // instead of one prefetch instruction per 128 bytes -- those brought in
   // single sectors, and a quarter of the demand loads still missed L2
   {
-    // (persistent CTAs: the group this CTA is likely to draw next -- tickets go
-    // round the resident CTAs roughly in turn; whoever draws it finds it in L2)
-    const unsigned ahead = kPersist ? gridDim.x : unsigned(P.prefetch_ctas);
-    long long en = e0 + static_cast<long long>(ahead) * EPB;
+    long long en = e0 + static_cast<long long>(P.prefetch_ctas) * EPB;
     if (P.groups) {
-      const unsigned nb = bid + ahead;
-      en = nb < P.n_groups ? static_cast<long long>(P.groups[nb]) * EPB : P.ne;
+      const unsigned nb = bid + unsigned(P.prefetch_ctas);
+      en = nb < gridDim.x ? static_cast<long long>(P.groups[nb]) * EPB : P.ne;
     }
     if (tid < 3 && en + EPB <= P.ne && (tid < 2 || read_out)) {
       const char* base = tid == 0   ? reinterpret_cast<const char*>(P.q + en * (5 * N3))
@@ -1085,8 +1025,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   {
     // the slabs have landed: every thread takes the raw values of its z line
     // out of the staging area, which the node values are about to overwrite
-    mbar_wait(mbar, ph0);
-    ph0 ^= 1u;
+    mbar_wait(mbar, 0);
     if (active) {
       const Real* sq = reinterpret_cast<const Real*>(smem_raw + off_q) + e * (5 * N3) + l;
       const Real* sp = reinterpret_cast<const Real*>(smem_raw + Map::kStagePhi + off_p) + e * N3 + l;
@@ -1185,10 +1124,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   ESDG_CLK();
 
   // the old `out` has had phase A to arrive in the slab
-  if (kBulk && read_out) {
-    mbar_wait(mbar + 1, ph1);
-    ph1 ^= 1u;
-  }
+  if (kBulk && read_out) mbar_wait(mbar + 1, 0);
   // ---- phase C: the six faces, thread per face node -----------------------
   // Every face subtracts its lift term from the shared tendency slab (zeroed
   // by the z-line owners in phase A). Faces of one direction share no node,
@@ -1310,10 +1246,6 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   for (int i = 0; i < NQ; ++i)
 #pragma unroll
     for (int v = 0; v < 5; ++v) acc[i][v] = Real(0);
-  // persistent CTAs: the number of the group after this one, drawn now so that
-  // the round trip of the atomic is over long before the commit needs it
-  unsigned nbid = bid + gridDim.x;
-  if (kPersist && P.ticket && tid == 0) nbid = atomicAdd(P.ticket, 1u) - P.ticket_base;
   if (VOL) {
 #ifdef ESDG_TUNE_UNROLL_DIR
 #pragma unroll
@@ -1361,7 +1293,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           // The thread that sweeps a line is the face node (s, t) of the
           // line's two faces: (l0, l1), for y lines (l1, l0).
           const int fn = dir == 1 ? ly1 + NQ * ly0 : l;
-          mbar_wait(mbar, ph0);
+          mbar_wait(mbar, (dir + 1) & 1);
           bool filled = true;
 #pragma unroll
           for (int v = 0; v < 5; ++v) {
@@ -1436,7 +1368,6 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
           }
         }
       }
-      if (kShare) ph0 ^= 1u; // this direction's copy of pulled terms has completed
       if (dir < 2) __syncthreads();
     }
   }
@@ -1459,10 +1390,6 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   const unsigned off_n =
       update ? unsigned(reinterpret_cast<unsigned long long>(P.q_next + slab0) & 15u) : 0u;
   Real knew[NQ][5], qc[NQ][5];
-#pragma unroll
-  for (int k = 0; k < NQ; ++k)
-#pragma unroll
-    for (int v = 0; v < 5; ++v) knew[k][v] = qc[k][v] = Real(0);
   if (active) {
     const Real* __restrict__ qe = P.q + eg * (5 * N3) + l;
     Real cf = Real(0);
@@ -1544,81 +1471,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
       }
     }
   }
-  // slab `which`: 0 = out from the tendency slab, 1 = q_next from `from` (bytes into smem)
-  const long long left_c = P.ne - e0;
-  const unsigned nel_c = left_c < EPB ? unsigned(left_c) : unsigned(EPB);
-  const unsigned bytes_c = nel_c * 5 * N3 * unsigned(sizeof(Real));
-  auto ship_slab = [&](int which, size_t from, bool interior) {
-    char* g = reinterpret_cast<char*>(which == 0 ? P.out + slab0 : P.q_next + slab0);
-    const char* sm = reinterpret_cast<const char*>(smem_raw) + from;
-    const unsigned head = (16u - unsigned(reinterpret_cast<unsigned long long>(g) & 15u)) & 15u;
-    const unsigned body = (bytes_c - head) & ~15u;
-    if (interior) {
-      bulk_s2g(g + head, sm + head, body);
-    } else {
-      for (unsigned o = 0; o < head; o += sizeof(Real))
-        *reinterpret_cast<Real*>(g + o) = *reinterpret_cast<const Real*>(sm + o);
-      for (unsigned o = head + body; o < bytes_c; o += sizeof(Real))
-        *reinterpret_cast<Real*>(g + o) = *reinterpret_cast<const Real*>(sm + o);
-    }
-  };
-  if (kBulk && kPersist) {
-    // Every z sweep is over: node values, the pulled terms' landing area and
-    // the table's place are dead, and the next group's loads go there while
-    // this group is committed. Both results leave through the slab, one after
-    // the other (k, then q_next once k has been read out of it), so that the
-    // node-value arrays are free for those loads.
-    // (q_next is formed now: one set of values, not q and k, lives through the first drain)
-    if (update && active) {
-#pragma unroll
-      for (int k = 0; k < NQ; ++k)
-#pragma unroll
-        for (int v = 0; v < 5; ++v) qc[k][v] = qc[k][v] + P.b_upd * knew[k][v];
-    }
-    __syncthreads();
-    if (tid == 0) {
-      *slot = nbid; // (the slot lies in the tail of the last node-value array)
-      if (nbid < P.n_groups) {
-        fence_proxy_async_smem(); // generic-proxy accesses of the arrays -> the copies' writes
-        issue_loads(group_start(nbid));
-      }
-    }
-    if (active) {
-#pragma unroll
-      for (int k = 0; k < NQ; ++k)
-#pragma unroll
-        for (int v = 0; v < 5; ++v) tslab[v * TV + zbase + k * ZS] = knew[k][v];
-    }
-    fence_proxy_async_smem(); // generic-proxy writes -> visible to the TMA engine
-    __syncthreads();
-    nbid = *slot;
-    if (tid == 0) {
-      ship_slab(0, Map::kTend + off_o, true);
-      bulk_store_commit_and_wait_read();
-    } else if (tid == 32) {
-      ship_slab(0, Map::kTend + off_o, false);
-    }
-    if (update) {
-      __syncthreads(); // k has been read out of the slab
-      Real* stage_n = reinterpret_cast<Real*>(smem_raw + Map::kTend + off_n);
-      if (active) {
-#pragma unroll
-        for (int k = 0; k < NQ; ++k)
-#pragma unroll
-          for (int v = 0; v < 5; ++v)
-            stage_n[(e * 5 + v) * N3 + l + k * N2] = qc[k][v];
-      }
-      fence_proxy_async_smem();
-      __syncthreads();
-      if (tid == 0) {
-        ship_slab(1, Map::kTend + off_n, true);
-        bulk_store_commit_and_wait_read();
-      } else if (tid == 32) {
-        ship_slab(1, Map::kTend + off_n, false);
-      }
-    }
-    __syncthreads(); // the slab is free for the next group
-  } else if (kBulk) {
+  if (kBulk) {
     // q_next goes where other threads may still be reading node values for
     // their z sweep: wait for them
     if (update) __syncthreads();
@@ -1640,27 +1493,42 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
     }
     fence_proxy_async_smem(); // generic-proxy writes -> visible to the TMA engine
     __syncthreads();
+    const long long left = P.ne - e0;
+    const unsigned nel = left < EPB ? unsigned(left) : unsigned(EPB);
+    const unsigned bytes = nel * 5 * N3 * unsigned(sizeof(Real));
+    // slab `which`: 0 = out from the tendency slab, 1 = q_next from the staging area
+    auto ship = [&](int which, bool interior) {
+      char* g = reinterpret_cast<char*>(which == 0 ? P.out + slab0 : P.q_next + slab0);
+      const char* sm = reinterpret_cast<const char*>(smem_raw) +
+                       (which == 0 ? Map::kTend + off_o : size_t(off_n));
+      const unsigned head = (16u - unsigned(reinterpret_cast<unsigned long long>(g) & 15u)) & 15u;
+      const unsigned body = (bytes - head) & ~15u;
+      if (interior) {
+        bulk_s2g(g + head, sm + head, body);
+      } else {
+        for (unsigned o = 0; o < head; o += sizeof(Real))
+          *reinterpret_cast<Real*>(g + o) = *reinterpret_cast<const Real*>(sm + o);
+        for (unsigned o = head + body; o < bytes; o += sizeof(Real))
+          *reinterpret_cast<Real*>(g + o) = *reinterpret_cast<const Real*>(sm + o);
+      }
+    };
     if (tid == 0) {
-      ship_slab(0, Map::kTend + off_o, true);
-      if (update) ship_slab(1, size_t(off_n), true);
+      ship(0, true);
+      if (update) ship(1, true);
       bulk_store_commit_and_wait_read();
     } else if (tid == 32) {
-      ship_slab(0, Map::kTend + off_o, false);
+      ship(0, false);
     } else if (tid == 64 && update) {
-      ship_slab(1, size_t(off_n), false);
+      ship(1, false);
     }
   }
 #ifdef ESDG_TUNE_PHASE_CLOCKS
   ESDG_CLK();
-  if (tid == 0 && bid == 40000u)
+  if (tid == 0 && blockIdx.x == 40000)
     printf("phase clocks VOL=%d SURF=%d: loads %lld | table barrier %lld | nodes %lld | barrier %lld | faces %lld | sweeps %lld | commit %lld | total %lld\n",
            int(VOL), int(SURF), tclk[1] - tclk[0], tclk[2] - tclk[1], tclk[3] - tclk[2], tclk[4] - tclk[3],
            tclk[5] - tclk[4], tclk[6] - tclk[5], tclk[7] - tclk[6], tclk[7] - tclk[0]);
 #endif
-  if (!kPersist) break;
-  bid = nbid;
-  first = false;
-  } // groups of a persistent CTA
 }
 
 // K3: q += b k (solver.hpp:342-353). Pure stream: 2 reads + 1 write per

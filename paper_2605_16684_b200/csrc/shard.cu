@@ -649,14 +649,9 @@ private:
     P.frec = frec_;
     P.epoch = epoch_;
     P.sync_error = flag_ + 1;
-    // the launch-order counter starts at zero in every launch (persistent CTAs
-    // draw one ticket more than they work on, so its end value is not known here)
     P.ticket = (share && use_ticket_) ? ticket_ : nullptr;
-    P.ticket_base = 0;
-    if (P.ticket) {
-      const cudaError_t e = cudaMemsetAsync(ticket_, 0, sizeof(unsigned), st);
-      if (e != cudaSuccess) return e;
-    }
+    P.ticket_base = ticket_base_;
+    if (P.ticket) ticket_base_ += unsigned((groups || n_groups > 0) ? n_groups : (ne_ + epb_ - 1) / epb_);
     P.wait_limit_ns = wait_limit_ns_;
     if (mode == kModeVolume && variant_ < 4 && !groups && n_groups == 0) {
       // a rung of the reference's ladder below "symmetric" (kernels.hpp:20-34)
@@ -798,6 +793,7 @@ private:
   int64_t frec_resets_ = 0;
   int share_faces_ = 1;
   unsigned* ticket_ = nullptr; // launch-order counter of the one-pass kernels
+  unsigned ticket_base_ = 0;
   int use_ticket_ = 1;
   unsigned long long wait_limit_ns_ = 2000000000ull;
   int variant_ = 5; // KernelVariant::Balanced
