@@ -562,7 +562,7 @@ def main_b200(args, rank, local_rank, world):
     }
 
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:     # the CPU leg belongs to the N=1 line only
         try:
             cpu = run_cpu_reference(args.order, args.precision, args.cpu_seconds)
             cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
