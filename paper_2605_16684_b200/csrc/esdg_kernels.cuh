@@ -769,7 +769,7 @@ struct FrecBlock {
 // written exactly once per evaluation (by the element across the face or by
 // its own element) before it is read, so "bit == this evaluation's parity"
 // means "filled", the slot needs no reset (15 global stores per thread and
-// 2.65 GB of writes per launch at configs[1] with the earlier NaN marker), and
+// 2.65 GB of L2 writes per launch at configs[1] with the earlier NaN marker), and
 // an 8-byte (4-byte) store being atomic, a value is either the previous
 // evaluation's or the new one. Clearing the bit truncates the term by at most
 // one ulp (1.1e-16 / 6e-8 relative, far inside the stated tolerances); the
