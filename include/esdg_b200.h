@@ -170,7 +170,13 @@ int esdg_b200_shard_stage_fused(esdg_b200_shard* s, double a_old, double a_new,
  * PART_BOUNDARY the rest. Order per RHS: pack -> start the transfer ->
  * PART_INTERIOR -> traces have landed -> PART_BOUNDARY. INTERIOR followed by
  * BOUNDARY is bitwise the PART_ALL result; stage_fused_part swaps the state
- * buffers after PART_BOUNDARY (or PART_ALL), so both parts read the old q. */
+ * buffers after PART_BOUNDARY (or PART_ALL), so both parts read the old q.
+ * PART_BOUNDARY belongs to the PART_INTERIOR launch before it, on the same
+ * stream: its groups take the lift terms of shared faces the interior groups
+ * left for them. (The shard tags those terms with the parity of the
+ * evaluation; a sequence that abandons an evaluation half way -- INTERIOR
+ * without its BOUNDARY -- is allowed, the next evaluation starts from
+ * re-initialised slots.) */
 enum {
   ESDG_B200_PART_ALL = 0,
   ESDG_B200_PART_INTERIOR = 1,
