@@ -298,11 +298,16 @@ template <int NQ, int BYTES> struct FlatXY { static constexpr bool value = NQ ==
 // FP64: +3 ... +10 % on the stage path) and loses where one or two fat CTAs
 // per SM ran the six faces as paired instruction streams (FPI = 2): there
 // halving the faces halves the work per iteration, not the latency of an
-// iteration (N = 6 FP64 -6 %, N = 7 FP32 -7 %); those tiles keep evaluating
-// all six faces of an element.
+// iteration (N = 6 FP64 -6 %, N = 7 FP32 -7 %; -3.4 % and -3 ... -4.5 % once the
+// lift terms were tagged and no slot had to be reset any more); those tiles
+// keep evaluating all six faces of an element.
 template <int NQ, int BYTES> struct Share { static constexpr bool value = true; };
-template <> struct Share<7, 8> { static constexpr bool value = false; };
-template <> struct Share<8, 4> { static constexpr bool value = false; };
+#ifndef ESDG_TUNE_SHARE78
+#define ESDG_TUNE_SHARE78 false
+#define ESDG_TUNE_SHARE84 false
+#endif
+template <> struct Share<7, 8> { static constexpr bool value = ESDG_TUNE_SHARE78; };
+template <> struct Share<8, 4> { static constexpr bool value = ESDG_TUNE_SHARE84; };
 template <> struct Tile<6, 8> : TilePick<ESDG_TUNE_T68E, ESDG_TUNE_T68M> { static constexpr int FPI = 2; static constexpr bool LEAN = false; };
 template <> struct Tile<7, 8> : TilePick<ESDG_TUNE_T78E, ESDG_TUNE_T78M> { static constexpr int FPI = 2; static constexpr bool LEAN = true; };
 template <> struct Tile<8, 8> { static constexpr int EPB = 1, MINB = 3; static constexpr int FPI = 2; static constexpr bool LEAN = true; };
