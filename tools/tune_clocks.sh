@@ -5,6 +5,6 @@ for spec in "$@"; do
   rm -f build/inst_nq5.o
   make -j8 EXTRA="$extra" > /dev/null 2>&1 || { echo "$name: build failed"; continue; }
   echo "== $name"
-  (cd ../.. && python tools/perf_probe.py --reps 1 2>&1 | grep "phase clocks" | sort | uniq -c | sort -rn | head -12)
+  (cd ../.. && python tools/perf_probe.py --reps 1 $PROBE_ARGS 2>&1 | grep "phase clocks" | sort | uniq -c | sort -rn | head -12)
 done
 rm -f build/inst_nq5.o; make -j8 > /dev/null 2>&1
