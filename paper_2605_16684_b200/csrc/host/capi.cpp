@@ -245,7 +245,8 @@ int esdg_b200_nccl_selftest(int device, int precision, int64_t count, int64_t* m
   bool ok = cudaMalloc(&d_send, bytes) == cudaSuccess && cudaMalloc(&d_recv, bytes) == cudaSuccess &&
             cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
             cudaMemcpy(d_send, h_send.data(), bytes, cudaMemcpyHostToDevice) == cudaSuccess &&
-            cudaMemset(d_recv, 0, bytes) == cudaSuccess;
+            cudaMemset(d_recv, 0, bytes) == cudaSuccess &&
+            cudaDeviceSynchronize() == cudaSuccess; // the exchange runs on a non-blocking stream
   if (ok) {
     // two peer blocks, both "peers" being this rank: what a partition with
     // two neighbours issues per RHS

@@ -258,6 +258,11 @@ public:
     CU(cudaMallocHost(&flag_host_, 2 * sizeof(unsigned long long)));
     CU(cudaMalloc(&flag_records_, sizeof(dev::FlagRecord) * dev::kFlagSlots));
     CU(cudaMemset(flag_records_, 0xff, sizeof(dev::FlagRecord) * dev::kFlagSlots));
+    // The copies and fills above went through the legacy stream, and a copy
+    // from pageable host memory returns once the data are STAGED, not once they
+    // are on the device; the kernels run on a non-blocking stream that the
+    // legacy stream does not order against.
+    CU(cudaDeviceSynchronize());
     return ESDG_B200_OK;
   }
 
@@ -270,10 +275,15 @@ public:
     if (async) {
       CU(cudaMemcpyAsync(dst, host, per * size_t(count), cudaMemcpyHostToDevice, pick(st)));
     } else {
-      // kernels run on a non-blocking stream the legacy stream does not order
-      // against: whatever still reads or writes the register must finish first
+      // On the compute stream itself, then wait: behind whatever still reads or
+      // writes the register, in front of every later kernel. (A blocking
+      // cudaMemcpy from pageable memory returns when the data are staged -- the
+      // DMA runs on the legacy stream, which the non-blocking compute stream
+      // does not wait for: a kernel launched right after could read a register
+      // that had not arrived yet. Seen as a rare gross mismatch of the
+      // accumulate form in tests/test_gpu_face_sharing.py.)
+      CU(cudaMemcpyAsync(dst, host, per * size_t(count), cudaMemcpyHostToDevice, stream_));
       CU(cudaStreamSynchronize(stream_));
-      CU(cudaMemcpy(dst, host, per * size_t(count), cudaMemcpyHostToDevice));
     }
     return ESDG_B200_OK;
   }
@@ -287,8 +297,8 @@ public:
     if (async) {
       CU(cudaMemcpyAsync(host, src, per * size_t(count), cudaMemcpyDeviceToHost, pick(st)));
     } else {
+      CU(cudaMemcpyAsync(host, src, per * size_t(count), cudaMemcpyDeviceToHost, stream_));
       CU(cudaStreamSynchronize(stream_));
-      CU(cudaMemcpy(host, src, per * size_t(count), cudaMemcpyDeviceToHost));
     }
     return ESDG_B200_OK;
   }
@@ -590,6 +600,7 @@ public:
       }
     }
     CU(cudaMemset(flag_records_, 0xff, sizeof(dev::FlagRecord) * dev::kFlagSlots));
+    CU(cudaDeviceSynchronize()); // (legacy-stream fill: in place before the next kernel of the compute stream)
     return ESDG_B200_NONPHYSICAL;
   }
 
