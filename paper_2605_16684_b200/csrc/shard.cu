@@ -642,10 +642,12 @@ private:
       P.lift[k] = lift_[k];
     }
     P.with_source = (with_source && coriolis_mode_ != 0) ? 1 : 0;
+    int epb_mode = epb_; // elements per CTA of THIS kernel (the split kernels may use another tile)
     {
       int threads = 0, epb = 0;
       size_t smem = 0;
       rhs_launch_shape<Real, NQ>(mode, &threads, &epb, &smem);
+      epb_mode = epb;
       const int per_sm = std::max(1, std::min(int(smem_per_sm_ / std::max<size_t>(smem, 1)), 2048 / std::max(threads, 1)));
       P.prefetch_ctas = sm_count_ * per_sm;
     }
@@ -662,7 +664,7 @@ private:
     P.sync_error = flag_ + 1;
     P.ticket = (share && use_ticket_) ? ticket_ : nullptr;
     P.ticket_base = ticket_base_;
-    if (P.ticket) ticket_base_ += unsigned((groups || n_groups > 0) ? n_groups : (ne_ + epb_ - 1) / epb_);
+    if (P.ticket) ticket_base_ += unsigned((groups || n_groups > 0) ? n_groups : (ne_ + epb_mode - 1) / epb_mode);
     P.wait_limit_ns = wait_limit_ns_;
     if (mode == kModeVolume && variant_ < 4 && !groups && n_groups == 0) {
       // a rung of the reference's ladder below "symmetric" (kernels.hpp:20-34)
