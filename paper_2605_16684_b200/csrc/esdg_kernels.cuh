@@ -1403,11 +1403,7 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
 #pragma unroll
       for (int k = 0; k < NQ; ++k)
 #pragma unroll
-#ifdef ESDG_TUNE_NO_QREAD
-        for (int v = 0; v < 5; ++v) qc[k][v] = Real(k + v);
-#else
         for (int v = 0; v < 5; ++v) qc[k][v] = qe[v * N3 + k * N2];
-#endif
     } else if (source) {
       // coriolis_source (physics.hpp:297-306) only needs the momenta
 #pragma unroll
