@@ -888,8 +888,24 @@ __global__ void __launch_bounds__(EPB* NQ* NQ, MINB)
   // thread <-> (element e, line l = l0 + NQ l1). In phase A, in the z sweep
   // and in the commit the thread owns the z line through (x, y) = (l0, l1),
   // so those three stages hand data over in registers.
-  const int e = tid / N2, l = tid - e * N2;
-  const int l0 = l % NQ, l1 = l / NQ;
+  // (element, x, y) of the thread. From NQ = 5 on they are packed in one opaque
+  // register: wherever the compiler prefers recomputing them to keeping them,
+  // that is a field extraction instead of two divisions of threadIdx.x by
+  // constants (stage path +0.7 ... +2.7 % at N = 4..7 where it is used; it
+  // loses 6 % at N = 2 FP32 and 0.5 % at N = 5 FP32, which keep the plain form)
+  // (and the volume-only kernel of N = 7 FP64, which spills either way: +4.5 %)
+  constexpr bool kPackedGeo =
+      NQ >= 5 && !(NQ == 6 && sizeof(Real) == 4) && !(NQ == 8 && sizeof(Real) == 8 && !SURF);
+  unsigned geo = 0;
+  if (kPackedGeo) {
+    const int e_ = tid / N2, l_ = tid - e_ * N2;
+    geo = unsigned(e_) | (unsigned(l_ % NQ) << 8) | (unsigned(l_ / NQ) << 16);
+    asm volatile("" : "+r"(geo));
+  }
+  const int e = kPackedGeo ? int(geo & 0xffu) : tid / N2;
+  const int l = kPackedGeo ? int((geo >> 8) & 0xffu) + NQ * int(geo >> 16) : tid - e * N2;
+  const int l0 = kPackedGeo ? int((geo >> 8) & 0xffu) : l % NQ;
+  const int l1 = kPackedGeo ? int(geo >> 16) : l / NQ;
   const long long eg = e0 + e;
   const bool active = eg < P.ne; // only the last CTA has idle lines
   // the y line this thread sweeps: its own element's (x, z) = (l0, l1), or any
