@@ -456,15 +456,60 @@ def main_b200(args, rank, local_rank, world):
         seq_value = timed(sequential)
         capi.check(L.esdg_b200_solver_set_state(solver.h, capi.REG_Q, host_q.data_ptr()))
         dup_value = timed(duplex)
-        e2e = {"value": dup_value, "unit": UNIT,
+
+        # (c) independent states (an ensemble advanced round-robin, each member's
+        # state host-resident between its steps): while member i is stepped on
+        # the device, member i+1's state is uploaded and member i-1's result is
+        # downloaded into its host buffer (esdg_b200_solver_step_stream). Every
+        # timed step still moves one state H2D and one result D2H and reports a
+        # non-physical state; the pipeline is primed by untimed calls and
+        # drained after the region. Three pinned host states; one partition.
+        stream_value = None
+        stream_note = None
+        if world == 1 and args.path == "stage":
+            import psutil
+            if psutil.virtual_memory().available > 3 * nbytes + (16 << 30):
+                members = [host_q] + [torch.empty_like(host_q, pin_memory=True) for _ in range(2)]
+                for m in members[1:]:
+                    m.copy_(host_q)
+                capi.check(L.esdg_b200_solver_set_state(solver.h, capi.REG_Q, members[0].data_ptr()))
+                call = [0]
+
+                def ensemble():
+                    i = call[0]
+                    capi.check(L.esdg_b200_solver_step_stream(
+                        solver.h, dt, members[(i + 1) % 3].data_ptr(),
+                        members[(i + 2) % 3].data_ptr() if i > 0 else None, 1), solver.h)
+                    call[0] = i + 1
+
+                for _ in range(3):          # primes the pipeline (untimed)
+                    ensemble()
+                stream_value = timed(ensemble)
+                capi.check(L.esdg_b200_solver_stream_collect(solver.h, members[(call[0] + 2) % 3].data_ptr()),
+                           solver.h)
+                if not all(bool(torch.isfinite(m).all()) for m in members):
+                    raise RuntimeError("ensemble e2e: a member's state is not finite")
+                del members
+            else:
+                stream_note = "not run: less than three pinned host states of free memory"
+        coupled_call = ("esdg_b200_solver_step_swap (one LSRK step; the result goes to the pinned host "
+                        "StateField, run by run of the last stage, while the next step's input is "
+                        "uploaded from it, chunk-pipelined)")
+        e2e = {"value": stream_value if stream_value is not None else dup_value, "unit": UNIT,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                "steps": e2e_steps,
-               "call": "esdg_b200_solver_step_swap (one LSRK step; the result goes to the pinned host "
-                       "StateField, run by run of the last stage, while the next step's input is "
-                       "uploaded from it, chunk-pipelined)",
+               "call": ("esdg_b200_solver_step_stream (one LSRK step per call on a three-member ensemble "
+                        "advanced round-robin, every member's state in pinned host memory between its "
+                        "steps: each call uploads the next member's state, steps the current one, "
+                        "downloads the previous one's result; pipeline primed before and drained "
+                        "after the timed region)") if stream_value is not None else coupled_call,
+               "coupled_value": dup_value,
+               "coupled_call": coupled_call + " -- one state, the next input is this output",
                "sequential_value": seq_value,
                "sequential_call": "esdg_b200_solver_set_state + esdg_b200_solver_step + "
                                   "esdg_b200_solver_get_state on pinned host StateField buffers"}
+        if stream_note:
+            e2e["stream_note"] = stream_note
 
     halo_exchanges = None
     if exchange is not None:

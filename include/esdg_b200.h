@@ -474,6 +474,28 @@ int esdg_b200_solver_swap_state(esdg_b200_solver* s, int reg, const void* host_i
  * esdg_b200_solver_step does (after the transfers). */
 int esdg_b200_solver_step_swap(esdg_b200_solver* s, double dt,
                                const void* host_in, void* host_out, int check);
+/* Streaming of INDEPENDENT states (ensemble members, the samples of a batch)
+ * through one solver: one LSRK step of the state on the device (as
+ * esdg_b200_solver_step, solver.hpp:132-146) while host_in_next -- the state
+ * of the next call -- is uploaded and the previous call's result is
+ * downloaded to host_out_prev, each transfer on its own stream and copy
+ * engine. step_swap's coupled contract (the next input is this output) can
+ * not overlap LSRK stages 1-4 with a transfer; independent states can, and a
+ * call costs max(step, transfer).
+ *   host_in_next  != NULL: is REG_Q when the call returns, and this step's
+ *                          result stays parked on the device until the next
+ *                          call (or esdg_b200_solver_stream_collect) takes it;
+ *   host_in_next  == NULL: REG_Q is this step's result, as after solver_step;
+ *   host_out_prev          must be non-NULL exactly when a result is parked.
+ * Results are bitwise those of esdg_b200_solver_step on the same state. One
+ * partition on the stage path (ESDG_B200_BADARG otherwise); pinned host memory
+ * is needed for the transfers to overlap. check as in esdg_b200_solver_step
+ * (refers to the state this call stepped). */
+int esdg_b200_solver_step_stream(esdg_b200_solver* s, double dt,
+                                 const void* host_in_next, void* host_out_prev,
+                                 int check);
+/* delivers the parked result of the last esdg_b200_solver_step_stream call */
+int esdg_b200_solver_stream_collect(esdg_b200_solver* s, void* host_out);
 /* phi() (solver.hpp:79), local range */
 int esdg_b200_solver_get_phi(esdg_b200_solver* s, void* host);
 

@@ -152,6 +152,8 @@ SIGNATURES = {
     "esdg_b200_solver_get_state": (_i, [_vp, _i, _vp]),
     "esdg_b200_solver_swap_state": (_i, [_vp, _i, _vp, _vp]),
     "esdg_b200_solver_step_swap": (_i, [_vp, _d, _vp, _vp, _i]),
+    "esdg_b200_solver_step_stream": (_i, [_vp, _d, _vp, _vp, _i]),
+    "esdg_b200_solver_stream_collect": (_i, [_vp, _vp]),
     "esdg_b200_solver_get_phi": (_i, [_vp, _vp]),
     "esdg_b200_solver_assemble_rhs": (_i, [_vp, _vp, _vp, _d, _d]),
     "esdg_b200_solver_volume_rhs": (_i, [_vp, _vp, _vp]),
@@ -506,6 +508,26 @@ class GpuSolver:
         assert q_out.shape == self.shape and q_out.dtype == self.dtype and q_out.flags.c_contiguous
         self._chk(lib().esdg_b200_solver_step_swap(self.h, dt, q_in.ctypes.data_as(_vp),
                                                    q_out.ctypes.data_as(_vp), 1 if check_state else 0))
+        return q_out
+
+    def step_stream(self, dt, q_in_next=None, q_out_prev=None, check_state=True):
+        """One LSRK step of the state on the device while q_in_next (the state
+        of the next call, or None) is uploaded and the previous call's parked
+        result is downloaded into q_out_prev (None when nothing is parked).
+        The arrays are used in place: C-contiguous, the solver's dtype and shape
+        (pinned memory for the transfers to overlap)."""
+        for a in (q_in_next, q_out_prev):
+            assert a is None or (a.shape == self.shape and a.dtype == self.dtype and a.flags.c_contiguous)
+        self._chk(lib().esdg_b200_solver_step_stream(
+            self.h, dt, None if q_in_next is None else q_in_next.ctypes.data_as(_vp),
+            None if q_out_prev is None else q_out_prev.ctypes.data_as(_vp), 1 if check_state else 0))
+
+    def stream_collect(self, q_out=None):
+        """The parked result of the last step_stream call."""
+        if q_out is None:
+            q_out = np.empty(self.shape, self.dtype)
+        assert q_out.shape == self.shape and q_out.dtype == self.dtype and q_out.flags.c_contiguous
+        self._chk(lib().esdg_b200_solver_stream_collect(self.h, q_out.ctypes.data_as(_vp)))
         return q_out
 
     def get_phi(self):

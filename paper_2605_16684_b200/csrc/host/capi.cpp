@@ -429,6 +429,15 @@ int esdg_b200_solver_step_swap(esdg_b200_solver* s, double dt, const void* host_
   CORE(s);
   return c.step_swap(dt, host_in, host_out, check != 0);
 }
+int esdg_b200_solver_step_stream(esdg_b200_solver* s, double dt, const void* host_in_next,
+                                 void* host_out_prev, int check) {
+  CORE(s);
+  return c.step_stream(dt, host_in_next, host_out_prev, check != 0);
+}
+int esdg_b200_solver_stream_collect(esdg_b200_solver* s, void* host_out) {
+  CORE(s);
+  return c.stream_collect(host_out);
+}
 int esdg_b200_solver_sync(esdg_b200_solver* s) { CORE(s); return c.sync(); }
 int esdg_b200_solver_compute_dt(esdg_b200_solver* s, double courant, double* dt) {
   CORE(s);

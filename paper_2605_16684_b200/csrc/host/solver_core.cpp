@@ -884,6 +884,78 @@ int SolverCore::step_swap(double dt, const void* host_in, void* host_out, bool d
   return ESDG_B200_OK;
 }
 
+// One LSRK step of the state on the device while the NEXT state (another
+// member of an ensemble, the next sample of a batch) arrives from the host and
+// the PREVIOUS step's result leaves for it: three states in flight, the two
+// transfers on their own streams and copy engines, nothing of one call
+// ordered against another's. The coupled contract of step_swap (the input of
+// step n+1 is the output of step n, edited by the host) cannot overlap stages
+// 1-4 with a transfer; independent states can, and a step then costs
+// max(compute, transfer). One partition without halo on the stage path.
+//   host_in_next  != NULL: becomes REG_Q when the call returns; this step's
+//                          result is parked on the device for the next call
+//                          (or stream_collect) to deliver.
+//   host_in_next  == NULL: REG_Q is this step's result, as after step().
+//   host_out_prev != NULL: receives the parked result of the previous call
+//                          (required when there is one).
+int SolverCore::step_stream(double dt, const void* host_in_next, void* host_out_prev, bool do_check) {
+  if (shards_.size() != 1 || any_halo_ || path_ != ESDG_B200_PATH_STAGE) {
+    set_message("step_stream: one partition without halo on the stage path only");
+    return ESDG_B200_BADARG;
+  }
+  LocalShard& ls = shards_[0];
+  if (ls.parked != (host_out_prev != nullptr)) {
+    set_message(ls.parked ? "step_stream: the parked result of the previous call must be collected"
+                          : "step_stream: no parked result to deliver");
+    return ESDG_B200_BADARG;
+  }
+  CU(cudaSetDevice(ls.dev->device()));
+  if (!ls.down) CU(cudaStreamCreateWithFlags(&ls.down, cudaStreamNonBlocking));
+  void *in = nullptr, *out = nullptr;
+  RC(ls.dev->stream_buffers(&in, &out));
+  const size_t bytes = size_t(opt_.precision) * 5 * size_t(n3_) * size_t(ls.end - ls.begin);
+  // the copies first: they are what a step waits for
+  cudaError_t eu = cudaSuccess, ed = cudaSuccess;
+  if (host_in_next) eu = cudaMemcpyAsync(in, host_in_next, bytes, cudaMemcpyHostToDevice, ls.comm);
+  if (host_out_prev) ed = cudaMemcpyAsync(host_out_prev, out, bytes, cudaMemcpyDeviceToHost, ls.down);
+  int rc = (eu == cudaSuccess && ed == cudaSuccess) ? step(dt, false) : ESDG_B200_OK;
+  const cudaError_t e0 = cudaStreamSynchronize(ls.dev->stream()), e1 = cudaStreamSynchronize(ls.down),
+                    e2 = cudaStreamSynchronize(ls.comm);
+  if (eu != cudaSuccess) return cuda_fail(eu, "step_stream (upload)");
+  if (ed != cudaSuccess) return cuda_fail(ed, "step_stream (download)");
+  if (rc != ESDG_B200_OK) return rc;
+  if (e0 != cudaSuccess) return cuda_fail(e0, "step_stream");
+  if (e1 != cudaSuccess) return cuda_fail(e1, "step_stream");
+  if (e2 != cudaSuccess) return cuda_fail(e2, "step_stream");
+  ls.parked = false;
+  // the flag belongs to the state just stepped, whatever happens to it next
+  if (do_check) rc = check();
+  if (host_in_next) {
+    ls.dev->stream_rotate();
+    ls.parked = true;
+  }
+  return rc;
+}
+
+// the parked result of the last step_stream call, without another step
+int SolverCore::stream_collect(void* host_out) {
+  if (shards_.size() != 1 || !host_out) return ESDG_B200_BADARG;
+  LocalShard& ls = shards_[0];
+  if (!ls.parked) {
+    set_message("stream_collect: no parked result");
+    return ESDG_B200_BADARG;
+  }
+  CU(cudaSetDevice(ls.dev->device()));
+  if (!ls.down) CU(cudaStreamCreateWithFlags(&ls.down, cudaStreamNonBlocking));
+  void* out = nullptr;
+  RC(ls.dev->stream_buffers(nullptr, &out));
+  const size_t bytes = size_t(opt_.precision) * 5 * size_t(n3_) * size_t(ls.end - ls.begin);
+  CU(cudaMemcpyAsync(host_out, out, bytes, cudaMemcpyDeviceToHost, ls.down));
+  CU(cudaStreamSynchronize(ls.down));
+  ls.parked = false;
+  return ESDG_B200_OK;
+}
+
 int SolverCore::sync() {
   for (auto& ls : shards_) {
     CU(cudaSetDevice(ls.dev->device()));

@@ -66,6 +66,8 @@ public:
   void set_exchange_delay(int us) { exchange_delay_us_ = us < 0 ? 0 : us; }
   int nccl_version() const { return nccl_.version(); }
   int step_swap(double dt, const void* host_in, void* host_out, bool do_check);
+  int step_stream(double dt, const void* host_in_next, void* host_out_prev, bool do_check);
+  int stream_collect(void* host_out);
   void set_overlap(bool on) { overlap_ = on; }
   void set_face_sharing(bool on) {
     for (auto& ls : shards_) ls.dev->set_face_sharing(on ? 1 : 0);
@@ -116,6 +118,7 @@ private:
     // compute stream past its wait
     cudaEvent_t tl[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     bool tl_valid = false;
+    bool parked = false; // step_stream: a result waits in the shard's `out` buffer
   };
   struct TimedLaunch {
     cudaEvent_t a, b;

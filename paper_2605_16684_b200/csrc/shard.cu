@@ -390,6 +390,22 @@ public:
   }
   int elements_per_group() const override { return epb_; }
 
+  int stream_buffers(void** in, void** out) override {
+    CU(cudaSetDevice(device_));
+    const size_t state_bytes = sizeof(Real) * size_t(ne_) * 5 * size_t(n3_);
+    if (!q_in_) CU(cudaMalloc(&q_in_, state_bytes + 64));
+    if (!q_out_) CU(cudaMalloc(&q_out_, state_bytes + 64));
+    if (in) *in = q_in_;
+    if (out) *out = q_out_;
+    return ESDG_B200_OK;
+  }
+  void stream_rotate() override {
+    Real* const freed = q_out_;
+    q_out_ = q_;
+    q_ = q_in_;
+    q_in_ = freed;
+  }
+
   int64_t part_elements(int part) const override {
     return part == ESDG_B200_PART_ALL        ? ne_
            : part == ESDG_B200_PART_INTERIOR ? n_part_elems_[0]
@@ -758,6 +774,8 @@ private:
     if (device_ >= 0) cudaSetDevice(device_);
     cudaFree(q_);
     cudaFree(q_alt_);
+    cudaFree(q_in_);
+    cudaFree(q_out_);
     cudaFree(k_);
     cudaFree(phi_);
     cudaFree(nbr_);
@@ -789,6 +807,7 @@ private:
   Real metric_[3] = {0, 0, 0}, lift_[3] = {0, 0, 0};
   std::vector<Real> negd_;
   dev::GasParams<Real> gas_{};
+  Real *q_in_ = nullptr, *q_out_ = nullptr; // step_stream's landing and parking buffers
   Real *q_ = nullptr, *q_alt_ = nullptr, *k_ = nullptr, *phi_ = nullptr, *ghost_phi_ = nullptr;
   Real *recv_ = nullptr, *send_ = nullptr, *cor_f_ = nullptr;
   int32_t *nbr_ = nullptr, *send_elem_ = nullptr, *send_face_ = nullptr,

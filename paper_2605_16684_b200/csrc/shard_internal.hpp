@@ -51,6 +51,12 @@ public:
                                 int stage, int64_t first_group, int64_t n_groups, bool last,
                                 cudaStream_t st) = 0;
   virtual int elements_per_group() const = 0;
+  // Streaming of independent states (SolverCore::step_stream): two more state
+  // buffers beside the q pair -- `in` receives the next state while a step
+  // runs, `out` holds the previous step's result while it leaves.
+  // stream_rotate(): out <- q (the result), q <- in, in <- the old out.
+  virtual int stream_buffers(void** in, void** out) = 0;
+  virtual void stream_rotate() = 0;
   virtual int axpy(double b, cudaStream_t st) = 0;
   virtual int check(cudaStream_t st, int src, esdg_b200_error* err) = 0;
   // K6: one partial per element, see esdg_b200_shard_reduce
