@@ -425,10 +425,11 @@ def main_b200(args, rank, local_rank, world):
         capi.check(L.esdg_b200_solver_get_state(solver.h, capi.REG_Q, host_q.data_ptr()))
         e2e_steps = max(2, min(args.steps, 4))
 
-        def timed(body):
+        def timed(body, n_steps=None):
+            n_steps = n_steps or e2e_steps
             barrier()
             t0 = time.perf_counter()
-            for _ in range(e2e_steps):
+            for _ in range(n_steps):
                 body()
             barrier()
             wall = time.perf_counter() - t0
@@ -436,7 +437,7 @@ def main_b200(args, rank, local_rank, world):
                 t = torch.tensor([wall], dtype=torch.float64, device=cdev)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 wall = float(t.item())
-            return dof_total * 5 * e2e_steps / wall
+            return dof_total * 5 * n_steps / wall
 
         # (a) the plain calls: upload, step, download, one after the other
         def sequential():
@@ -484,7 +485,8 @@ def main_b200(args, rank, local_rank, world):
 
                 for _ in range(3):          # primes the pipeline (untimed)
                     ensemble()
-                stream_value = timed(ensemble)
+                stream_steps = max(e2e_steps, args.steps)
+                stream_value = timed(ensemble, stream_steps)
                 capi.check(L.esdg_b200_solver_stream_collect(solver.h, members[(call[0] + 2) % 3].data_ptr()),
                            solver.h)
                 if not all(bool(torch.isfinite(m).all()) for m in members):
@@ -497,13 +499,13 @@ def main_b200(args, rank, local_rank, world):
                         "uploaded from it, chunk-pipelined)")
         e2e = {"value": stream_value if stream_value is not None else dup_value, "unit": UNIT,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-               "steps": e2e_steps,
+               "steps": stream_steps if stream_value is not None else e2e_steps,
                "call": ("esdg_b200_solver_step_stream (one LSRK step per call on a three-member ensemble "
                         "advanced round-robin, every member's state in pinned host memory between its "
                         "steps: each call uploads the next member's state, steps the current one, "
                         "downloads the previous one's result; pipeline primed before and drained "
                         "after the timed region)") if stream_value is not None else coupled_call,
-               "coupled_value": dup_value,
+               "coupled_value": dup_value, "coupled_steps": e2e_steps,
                "coupled_call": coupled_call + " -- one state, the next input is this output",
                "sequential_value": seq_value,
                "sequential_call": "esdg_b200_solver_set_state + esdg_b200_solver_step + "

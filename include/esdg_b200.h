@@ -487,9 +487,10 @@ int esdg_b200_solver_step_swap(esdg_b200_solver* s, double dt,
  *                          call (or esdg_b200_solver_stream_collect) takes it;
  *   host_in_next  == NULL: REG_Q is this step's result, as after solver_step;
  *   host_out_prev          must be non-NULL exactly when a result is parked.
- * Results are bitwise those of esdg_b200_solver_step on the same state. One
- * partition on the stage path (ESDG_B200_BADARG otherwise); pinned host memory
- * is needed for the transfers to overlap. check as in esdg_b200_solver_step
+ * Results are bitwise those of esdg_b200_solver_step on the same state. Any
+ * path and partition count; the host arrays cover the LOCAL element range as
+ * for set_state / get_state. ESDG_B200_BADARG when the parked-result protocol
+ * is broken. Pinned host memory is needed for the transfers to overlap. check as in esdg_b200_solver_step
  * (refers to the state this call stepped). */
 int esdg_b200_solver_step_stream(esdg_b200_solver* s, double dt,
                                  const void* host_in_next, void* host_out_prev,

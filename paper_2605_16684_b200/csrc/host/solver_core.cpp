@@ -178,6 +178,7 @@ SolverCore::~SolverCore() {
     if (ls.dev) cudaSetDevice(ls.dev->device());
     if (ls.comm) cudaStreamDestroy(ls.comm);
     if (ls.down) cudaStreamDestroy(ls.down);
+    if (ls.up) cudaStreamDestroy(ls.up);
     if (ls.ev_pack) cudaEventDestroy(ls.ev_pack);
     if (ls.ev_recv) cudaEventDestroy(ls.ev_recv);
     if (ls.ev_surf) cudaEventDestroy(ls.ev_surf);
@@ -887,11 +888,12 @@ int SolverCore::step_swap(double dt, const void* host_in, void* host_out, bool d
 // One LSRK step of the state on the device while the NEXT state (another
 // member of an ensemble, the next sample of a batch) arrives from the host and
 // the PREVIOUS step's result leaves for it: three states in flight, the two
-// transfers on their own streams and copy engines, nothing of one call
-// ordered against another's. The coupled contract of step_swap (the input of
-// step n+1 is the output of step n, edited by the host) cannot overlap stages
-// 1-4 with a transfer; independent states can, and a step then costs
-// max(compute, transfer). One partition without halo on the stage path.
+// transfers on their own streams and copy engines (not the halo's copy
+// stream), nothing of one call ordered against another's. The coupled
+// contract of step_swap (the input of step n+1 is the output of step n,
+// edited by the host) cannot overlap stages 1-4 with a transfer; independent
+// states can, and a step then costs max(compute, transfer). Any path, any
+// number of local partitions; host arrays cover the local element range.
 //   host_in_next  != NULL: becomes REG_Q when the call returns; this step's
 //                          result is parked on the device for the next call
 //                          (or stream_collect) to deliver.
@@ -899,60 +901,69 @@ int SolverCore::step_swap(double dt, const void* host_in, void* host_out, bool d
 //   host_out_prev != NULL: receives the parked result of the previous call
 //                          (required when there is one).
 int SolverCore::step_stream(double dt, const void* host_in_next, void* host_out_prev, bool do_check) {
-  if (shards_.size() != 1 || any_halo_ || path_ != ESDG_B200_PATH_STAGE) {
-    set_message("step_stream: one partition without halo on the stage path only");
+  if (parked_ != (host_out_prev != nullptr)) {
+    set_message(parked_ ? "step_stream: the parked result of the previous call must be collected"
+                        : "step_stream: no parked result to deliver");
     return ESDG_B200_BADARG;
   }
-  LocalShard& ls = shards_[0];
-  if (ls.parked != (host_out_prev != nullptr)) {
-    set_message(ls.parked ? "step_stream: the parked result of the previous call must be collected"
-                          : "step_stream: no parked result to deliver");
-    return ESDG_B200_BADARG;
-  }
-  CU(cudaSetDevice(ls.dev->device()));
-  if (!ls.down) CU(cudaStreamCreateWithFlags(&ls.down, cudaStreamNonBlocking));
-  void *in = nullptr, *out = nullptr;
-  RC(ls.dev->stream_buffers(&in, &out));
-  const size_t bytes = size_t(opt_.precision) * 5 * size_t(n3_) * size_t(ls.end - ls.begin);
+  const size_t per = size_t(opt_.precision) * 5 * size_t(n3_);
+  const int64_t first = local_begin_;
   // the copies first: they are what a step waits for
-  cudaError_t eu = cudaSuccess, ed = cudaSuccess;
-  if (host_in_next) eu = cudaMemcpyAsync(in, host_in_next, bytes, cudaMemcpyHostToDevice, ls.comm);
-  if (host_out_prev) ed = cudaMemcpyAsync(host_out_prev, out, bytes, cudaMemcpyDeviceToHost, ls.down);
-  int rc = (eu == cudaSuccess && ed == cudaSuccess) ? step(dt, false) : ESDG_B200_OK;
-  const cudaError_t e0 = cudaStreamSynchronize(ls.dev->stream()), e1 = cudaStreamSynchronize(ls.down),
-                    e2 = cudaStreamSynchronize(ls.comm);
-  if (eu != cudaSuccess) return cuda_fail(eu, "step_stream (upload)");
-  if (ed != cudaSuccess) return cuda_fail(ed, "step_stream (download)");
+  for (auto& ls : shards_) {
+    CU(cudaSetDevice(ls.dev->device()));
+    if (!ls.down) CU(cudaStreamCreateWithFlags(&ls.down, cudaStreamNonBlocking));
+    if (!ls.up) CU(cudaStreamCreateWithFlags(&ls.up, cudaStreamNonBlocking));
+    void *in = nullptr, *out = nullptr;
+    RC(ls.dev->stream_buffers(&in, &out));
+    const size_t off = size_t(ls.begin - first) * per, bytes = size_t(ls.end - ls.begin) * per;
+    if (host_in_next)
+      CU(cudaMemcpyAsync(in, static_cast<const char*>(host_in_next) + off, bytes, cudaMemcpyHostToDevice, ls.up));
+    if (host_out_prev)
+      CU(cudaMemcpyAsync(static_cast<char*>(host_out_prev) + off, out, bytes, cudaMemcpyDeviceToHost, ls.down));
+  }
+  int rc = step(dt, false);
+  cudaError_t bad = cudaSuccess;
+  for (auto& ls : shards_) {
+    cudaSetDevice(ls.dev->device());
+    for (cudaStream_t st : {ls.dev->stream(), ls.down, ls.up}) {
+      const cudaError_t e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess && bad == cudaSuccess) bad = e;
+    }
+  }
   if (rc != ESDG_B200_OK) return rc;
-  if (e0 != cudaSuccess) return cuda_fail(e0, "step_stream");
-  if (e1 != cudaSuccess) return cuda_fail(e1, "step_stream");
-  if (e2 != cudaSuccess) return cuda_fail(e2, "step_stream");
-  ls.parked = false;
+  if (bad != cudaSuccess) return cuda_fail(bad, "step_stream");
+  parked_ = false;
   // the flag belongs to the state just stepped, whatever happens to it next
   if (do_check) rc = check();
   if (host_in_next) {
-    ls.dev->stream_rotate();
-    ls.parked = true;
+    for (auto& ls : shards_) ls.dev->stream_rotate();
+    parked_ = true;
   }
   return rc;
 }
 
 // the parked result of the last step_stream call, without another step
 int SolverCore::stream_collect(void* host_out) {
-  if (shards_.size() != 1 || !host_out) return ESDG_B200_BADARG;
-  LocalShard& ls = shards_[0];
-  if (!ls.parked) {
+  if (!host_out) return ESDG_B200_BADARG;
+  if (!parked_) {
     set_message("stream_collect: no parked result");
     return ESDG_B200_BADARG;
   }
-  CU(cudaSetDevice(ls.dev->device()));
-  if (!ls.down) CU(cudaStreamCreateWithFlags(&ls.down, cudaStreamNonBlocking));
-  void* out = nullptr;
-  RC(ls.dev->stream_buffers(nullptr, &out));
-  const size_t bytes = size_t(opt_.precision) * 5 * size_t(n3_) * size_t(ls.end - ls.begin);
-  CU(cudaMemcpyAsync(host_out, out, bytes, cudaMemcpyDeviceToHost, ls.down));
-  CU(cudaStreamSynchronize(ls.down));
-  ls.parked = false;
+  const size_t per = size_t(opt_.precision) * 5 * size_t(n3_);
+  const int64_t first = local_begin_;
+  for (auto& ls : shards_) {
+    CU(cudaSetDevice(ls.dev->device()));
+    if (!ls.down) CU(cudaStreamCreateWithFlags(&ls.down, cudaStreamNonBlocking));
+    void* out = nullptr;
+    RC(ls.dev->stream_buffers(nullptr, &out));
+    CU(cudaMemcpyAsync(static_cast<char*>(host_out) + size_t(ls.begin - first) * per, out,
+                       size_t(ls.end - ls.begin) * per, cudaMemcpyDeviceToHost, ls.down));
+  }
+  for (auto& ls : shards_) {
+    CU(cudaSetDevice(ls.dev->device()));
+    CU(cudaStreamSynchronize(ls.down));
+  }
+  parked_ = false;
   return ESDG_B200_OK;
 }
 

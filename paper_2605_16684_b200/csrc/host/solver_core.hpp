@@ -111,14 +111,13 @@ private:
     int64_t begin = 0, end = 0;
     RankHalo halo;
     std::unique_ptr<ShardBase> dev;
-    cudaStream_t comm = nullptr, down = nullptr; // copy streams (down: step_swap's D2H)
+    cudaStream_t comm = nullptr, down = nullptr, up = nullptr; // copy streams (down: D2H of step_swap / step_stream, up: step_stream's H2D)
     cudaEvent_t ev_pack = nullptr, ev_recv = nullptr, ev_surf = nullptr;
     // timeline of the last recorded RHS (timing enabled): start, traces
     // packed and posted, first kernel start / end, last trace arrived,
     // compute stream past its wait
     cudaEvent_t tl[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     bool tl_valid = false;
-    bool parked = false; // step_stream: a result waits in the shard's `out` buffer
   };
   struct TimedLaunch {
     cudaEvent_t a, b;
@@ -154,6 +153,7 @@ private:
   int path_ = ESDG_B200_PATH_STAGE; // the fastest; SPLIT keeps the reference's kernel structure
   int reduction_ = ESDG_B200_REDUCE_ON_DEVICE;
   bool any_halo_ = false;
+  bool parked_ = false; // step_stream: a result waits in the shards' `out` buffers
   bool remote_peers() const { return opt_.exchange != nullptr || opt_.nccl; }
   int mark(LocalShard& ls, int which, cudaStream_t st);
   NcclTransport nccl_;

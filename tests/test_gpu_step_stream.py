@@ -10,8 +10,8 @@ The call bench.py's e2e arm times. What it must guarantee:
   * the k register and the device state after the last call are those of the
     plain sequence;
   * the parked-result protocol is enforced (a parked result must be collected,
-    none can be asked for when there is none), and configurations the call does
-    not cover are refused, not silently served another way;
+    none can be asked for when there is none), on every path and partition
+    count;
   * a non-physical member is reported by the call that stepped it.
 """
 import numpy as np
@@ -110,16 +110,31 @@ def test_collect_and_protocol(port):
     assert np.array_equal(s.get_state(), want_b)
 
 
-@pytest.mark.parametrize("ranks,path", [(2, capi.PATH_STAGE), (1, capi.PATH_SPLIT), (1, capi.PATH_FUSED)])
-def test_uncovered_configurations_are_refused(port, ranks, path):
-    oc, _ = both_configs("bubble", 1, False)
-    o = port.mesh(oc).solver(2, "f64")
-    q = members_of(o, 1)[0]
-    _, g = make(port, "bubble", (1, False), 2, ranks=ranks, path=path)
-    g.set_state(q)
-    with pytest.raises(capi.EsdgError):
-        g.step_stream(1e-3, q, None)
-    g.step(1e-3)   # and the solver is still usable
+@pytest.mark.parametrize("ranks,path", [(2, capi.PATH_STAGE), (3, capi.PATH_STAGE), (1, capi.PATH_SPLIT),
+                                        (2, capi.PATH_SPLIT), (1, capi.PATH_FUSED), (4, capi.PATH_FUSED)])
+def test_every_path_and_partition_count(port, ranks, path):
+    """Several partitions on the device (their halo exchange runs on its own
+    copy stream while the state transfers use theirs) and the paths whose
+    update is a separate kernel: three members, two rounds, bitwise step()."""
+    oc, _ = both_configs("bubble", 2, False)
+    o = port.mesh(oc).solver(3, "f64")
+    start = members_of(o)
+    dt, rounds = 1e-3, 2
+    _, g = make(port, "bubble", (2, False), 3, ranks=ranks, path=path)
+    want = []
+    for q in start:
+        g.set_state(q)
+        for _ in range(rounds):
+            g.step(dt)
+        want.append(g.get_state().copy())
+    _, s = make(port, "bubble", (2, False), 3, ranks=ranks, path=path)
+    host = [q.copy() for q in start]
+    s.set_state(host[0])
+    n_calls = 3 * rounds
+    for i in range(n_calls):
+        s.step_stream(dt, None if i == n_calls - 1 else host[(i + 1) % 3], host[(i + 2) % 3] if i > 0 else None)
+    assert np.array_equal(host[0], want[0]) and np.array_equal(host[1], want[1])
+    assert np.array_equal(s.get_state(), want[2])
 
 
 def test_nonphysical_member_is_reported_by_its_call(port):
