@@ -467,7 +467,7 @@ def main_b200(args, rank, local_rank, world):
         # drained after the region. Three pinned host states; one partition.
         stream_value = None
         stream_note = None
-        if world == 1 and args.path == "stage":
+        if world == 1:
             import psutil
             if psutil.virtual_memory().available > 3 * nbytes + (16 << 30):
                 members = [host_q] + [torch.empty_like(host_q, pin_memory=True) for _ in range(2)]
