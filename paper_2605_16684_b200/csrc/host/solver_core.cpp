@@ -269,7 +269,20 @@ int SolverCore::build_shard(LocalShard& ls) {
   RC(create_shard(d, &dev));
   ls.dev.reset(dev);
   CU(cudaSetDevice(d.device));
-  CU(cudaStreamCreateWithFlags(&ls.comm, cudaStreamNonBlocking));
+  {
+    // The halo's stream outranks the compute stream: the interior kernel is a
+    // grid of ~1e5 CTAs that fills every SM to its register limit, and a
+    // send/receive kernel of NCCL queued beside it at equal priority would get
+    // an SM only when that grid has been dealt out -- i.e. the exchange would
+    // follow the kernel it is meant to hide behind. With a higher priority its
+    // few CTAs take the next resources that come free.
+    int least = 0, greatest = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    // ESDG_B200_COMM_PRIORITY=0 (development): equal priority, for A/B runs
+    const char* env = std::getenv("ESDG_B200_COMM_PRIORITY");
+    CU(cudaStreamCreateWithPriority(&ls.comm, cudaStreamNonBlocking,
+                                    (env && env[0] == '0') ? least : greatest));
+  }
   CU(cudaEventCreateWithFlags(&ls.ev_pack, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&ls.ev_recv, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&ls.ev_surf, cudaEventDisableTiming));
