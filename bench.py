@@ -52,6 +52,11 @@ def parse_args():
                     choices=["weak", "strong"],
                     help="weak: BASELINE.json configs[4], ~1e8 DOF per GPU (bubble); strong: configs[3], "
                          "the fixed 3,145,728-element (~4e8 DOF) baroclinic channel cut into --gpus parts")
+    ap.add_argument("--overlap", default="auto", choices=["auto", "on", "off"],
+                    help="N > 1: interior element groups run while the traces travel (on), or the "
+                         "kernel waits for them and runs as one launch (off); auto times two steps "
+                         "of each after the warm-up and keeps the faster (the two launches cost "
+                         "2.5-5.6 %% of a step, an NVLink exchange tens of microseconds)")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "torch"],
                     help="N > 1: ncclSend/ncclRecv issued by the library (default) or the "
                          "torch.distributed callback (halo.py)")
@@ -353,6 +358,27 @@ def main_b200(args, rank, local_rank, world):
     for _ in range(max(args.warmup, 3)):
         solver.step(dt, check_state=True)
     solver.sync()
+    overlap_choice = None
+    if world > 1:
+        probe = {}
+        modes = ["on", "off"] if args.overlap == "auto" else [args.overlap]
+        for mode in modes:
+            solver.set_overlap(mode == "on")
+            solver.step(dt, check_state=True)          # settle the mode's launch lists
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(2):
+                solver.step(dt, check_state=True)
+            barrier()
+            t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=cdev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)      # every rank sees the same number
+            probe[mode] = float(t.item()) * 1e3 / 2
+        best = min(probe, key=probe.get)
+        solver.set_overlap(best == "on")
+        solver.step(dt, check_state=True)
+        solver.sync()
+        overlap_choice = {"mode": best, "selected_by": args.overlap,
+                          "probe_ms_per_step": {k: round(v, 3) for k, v in probe.items()}}
 
     # ---- timed region: exactly K steps, device events, max over ranks -----
     # A pass whose clock samples show a hardware or thermal slowdown, or SM
@@ -407,11 +433,19 @@ def main_b200(args, rank, local_rank, world):
 
     # one more step with the RankEvents timeline on (exchange.hpp:83-89):
     # did the first kernel of the last RHS start before its last trace arrived?
+    # (taken with the overlap on, whichever order the timed region ran in)
+    if world > 1 and overlap_choice["mode"] != "on":
+        solver.set_overlap(True)
+        solver.step(dt, check_state=True)
     solver.record_events(True)
     solver.step(dt, check_state=True)
     solver.sync()
     events = solver.rank_events()
     solver.record_events(False)
+    if world > 1 and overlap_choice["mode"] != "on":
+        solver.set_overlap(False)
+        solver.step(dt, check_state=True)
+        solver.sync()
     halo_bytes = solver.halo_bytes
     interior_el, local_el = solver.overlap_elements()
 
@@ -650,6 +684,7 @@ def main_b200(args, rank, local_rank, world):
             "halo_bytes_per_rhs": halo_bytes,
             "interior_fraction": interior_el / max(local_el, 1),
             "interior_elements": interior_el, "local_elements": local_el,
+            "overlap": overlap_choice,
             "events_ns": events,
             "interior_kernel_started_before_last_recv": events["volume_start_ns"] <= events["last_arrival_ns"],
         }

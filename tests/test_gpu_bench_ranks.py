@@ -54,6 +54,9 @@ def test_bench_two_ranks_one_gpu(scaling):
     assert abs(halo["local_elements"] - cfg["elements"] / 2) <= 1
     assert halo["halo_bytes_per_rhs"] > 0 and halo["exchanges"] > 0
     assert halo["interior_kernel_started_before_last_recv"] in (True, False)
+    # the order of kernel and exchange was chosen by timing both after the warm-up
+    assert halo["overlap"]["selected_by"] == "auto" and halo["overlap"]["mode"] in ("on", "off")
+    assert set(halo["overlap"]["probe_ms_per_step"]) == {"on", "off"}
     assert line["value"] > 0 and line["ms_per_step"] > 0
     assert line["gpu_launches"] >= 2 * 5
     assert line["e2e"]["value"] > 0
@@ -68,3 +71,12 @@ def test_bench_falls_back_when_nccl_cannot_pair_the_ranks():
     halo = line["config"]["halo"]
     assert 0 < halo["local_elements"] < line["config"]["elements"]
     assert "torch.distributed" in halo["exchange"]
+
+
+def test_bench_overlap_switch():
+    """--overlap off: the kernel waits for the traces and runs as one launch;
+    the event timeline of the report is still taken with the overlap on."""
+    line = _run(2, ["--exchange", "torch", "--overlap", "off"])
+    ov = line["config"]["halo"]["overlap"]
+    assert ov["mode"] == "off" and ov["selected_by"] == "off" and set(ov["probe_ms_per_step"]) == {"off"}
+    assert line["value"] > 0
