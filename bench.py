@@ -52,6 +52,9 @@ def parse_args():
                     choices=["weak", "strong"],
                     help="weak: BASELINE.json configs[4], ~1e8 DOF per GPU (bubble); strong: configs[3], "
                          "the fixed 3,145,728-element (~4e8 DOF) baroclinic channel cut into --gpus parts")
+    ap.add_argument("--no-stream-e2e", action="store_true",
+                    help="e2e: skip the streamed three-member ensemble (three pinned host states "
+                         "per rank), report the coupled step_swap figure as e2e.value")
     ap.add_argument("--overlap", default="auto", choices=["auto", "on", "off"],
                     help="N > 1: interior element groups run while the traces travel (on), or the "
                          "kernel waits for them and runs as one launch (off); auto times two steps "
@@ -498,12 +501,20 @@ def main_b200(args, rank, local_rank, world):
         # downloaded into its host buffer (esdg_b200_solver_step_stream). Every
         # timed step still moves one state H2D and one result D2H and reports a
         # non-physical state; the pipeline is primed by untimed calls and
-        # drained after the region. Three pinned host states; one partition.
+        # drained after the region. Three pinned host states per rank; with
+        # N ranks every rank streams its own Morton range of each member (the
+        # halo exchange of the step keeps its own copy stream) and all ranks
+        # decide together whether the host has the memory for it.
         stream_value = None
         stream_note = None
-        if world == 1:
+        if not args.no_stream_e2e:
             import psutil
-            if psutil.virtual_memory().available > 3 * nbytes + (16 << 30):
+            enough = psutil.virtual_memory().available > world * 3 * nbytes + (16 << 30) * (2 if world > 1 else 1)
+            if world > 1:
+                t = torch.tensor([1 if enough else 0], dtype=torch.int32, device=cdev)
+                dist.all_reduce(t, op=dist.ReduceOp.MIN)
+                enough = bool(int(t.item()))
+            if enough:
                 members = [host_q] + [torch.empty_like(host_q, pin_memory=True) for _ in range(2)]
                 for m in members[1:]:
                     m.copy_(host_q)

@@ -59,7 +59,9 @@ def test_bench_two_ranks_one_gpu(scaling):
     assert set(halo["overlap"]["probe_ms_per_step"]) == {"on", "off"}
     assert line["value"] > 0 and line["ms_per_step"] > 0
     assert line["gpu_launches"] >= 2 * 5
-    assert line["e2e"]["value"] > 0
+    assert line["e2e"]["value"] > 0 and line["e2e"]["coupled_value"] > 0
+    # every rank streams its own Morton range of the ensemble's members
+    assert "step_stream" in line["e2e"]["call"]
     assert line["e2e"]["h2d_bytes_per_step"] == halo["local_elements"] * 5 * (cfg["order"] + 1) ** 3 * 8
 
 
