@@ -372,6 +372,33 @@ public:
 #endif
   }
 
+  // Extension (no counterpart in the reference): independent states streamed
+  // through the solver. step(dt) of the state on the device while `next` (the
+  // state of the following call, or nullptr) is uploaded and the previous
+  // call's result is downloaded into `prev` (nullptr exactly when nothing is
+  // parked, i.e. on the first call of a stream) -- esdg_b200_solver_step_stream.
+  // After a call with next == nullptr, state() is this step's result; the
+  // parked result of a call with next != nullptr is taken by the next call or
+  // by stream_collect(). Fields are caller-owned, sized like state().
+  void step_stream(Real dt, const Field* next, Field* prev) {
+    sync_settings();
+    restore_internal();
+    push_if_needed();
+    const std::size_t n = std::size_t(ne_) * kNumVars * std::size_t(n3_);
+    if ((next && next->data.size() != n) || (prev && prev->data.size() != n))
+      throw std::invalid_argument("GpuSolver::step_stream: field size");
+    guard(esdg_b200_solver_step_stream(solver_, double(dt), next ? next->data.data() : nullptr,
+                                       prev ? prev->data.data() : nullptr, 1));
+    host_valid_ = false;
+    count_ops(true, 5);
+  }
+  void stream_collect(Field& out) {
+    out.n_elements = ne_;
+    out.nodes_per_element = n3_;
+    out.data.resize(std::size_t(ne_) * kNumVars * std::size_t(n3_));
+    check(esdg_b200_solver_stream_collect(solver_, out.data.data()));
+  }
+
   // compute_dt(courant) (solver.hpp:148-150)
   double compute_dt(double courant) const {
     restore_internal();

@@ -153,6 +153,29 @@ static void parity_and_partitions() {
     }
     CHECK(sf.state_view().data == ss.state_view().data);
   }
+  {
+    // step_stream: three members advanced round-robin (the next member's state
+    // arrives and the previous member's result leaves while one is stepped),
+    // bitwise the plain step() of each member
+    GpuSolver<double> plain(mc, 3, GasConstants{}, KernelSettings{}, 1);
+    GpuSolver<double> stream(mc, 3, GasConstants{}, KernelSettings{}, 1);
+    plain.set_path(ESDG_B200_PATH_STAGE);
+    stream.set_path(ESDG_B200_PATH_STAGE);
+    std::vector<esdg_b200::StateField<double>> member(3, q), want(3, q);
+    for (int m = 0; m < 3; ++m) {
+      for (auto& x : member[m].data) x *= 1.0 + 0.001 * m;
+      plain.state().data = member[m].data;
+      plain.step(dt);
+      plain.step(dt);
+      want[m].data = plain.state_view().data;
+    }
+    stream.state().data = member[0].data;
+    for (int i = 0; i < 6; ++i)
+      stream.step_stream(dt, i == 5 ? nullptr : &member[(i + 1) % 3], i ? &member[(i + 2) % 3] : nullptr);
+    CHECK(member[0].data == want[0].data);
+    CHECK(member[1].data == want[1].data);
+    CHECK(stream.state_view().data == want[2].data);
+  }
   CHECK(dmax <= 1e-12 * qmax);
   CHECK(std::fabs(s1.compute_dt(0.5) - orc_compute_dt_f64(o, 0.5)) <= 1e-12 * orc_compute_dt_f64(o, 0.5));
   {
