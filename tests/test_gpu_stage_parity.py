@@ -18,7 +18,8 @@ import pytest
 
 from oracle import pyoracle as po
 from paper_2605_16684_b200 import capi
-from helpers import both_configs, check_samples, face_table, sample_ranges, scaled_error, state_error
+from helpers import (both_configs, check_samples, face_table, gas_pair, sample_ranges, scaled_error,
+                     settings_pair, state_error)
 from test_gpu_parity import TOL32, TOL64, make
 
 pytestmark = pytest.mark.gpu
@@ -199,3 +200,32 @@ def test_sweep_size_sampled_parity(port, order, base, refinement, prec):
           f"{d_gpu:.2e}, f32 oracle vs f64 {d_or32:.2e}, GPU f32 vs f32 oracle {d_pair:.2e} "
           f"(GPU f64 vs f64 oracle {d_truth:.2e})")
     assert d_gpu <= max(TOL32, 1.5 * d_or32)
+
+
+def test_channel_size_sampled_parity(port):
+    """BASELINE.json configs[2] as bench.py --case baroclinic runs it: channel
+    mesh (12, 2, 1) at refinement 5 = 786,432 elements, N = 4 FP64 (98.3 MDOF),
+    beta-plane Coriolis, dissipation on, walls in y and z, periodic in x; the
+    perturbed balanced jet plus a rough 1e-3 modulation. One assemble_rhs on
+    the stage path; the oracle (same Coriolis settings) on sampled elements."""
+    cor = (2, 1e-4, 1.6e-11, 3e6)
+    margs = ((12, 2, 1), 5, (0., 0., 0.), (4e7, 6e6, 3e4), (0, 1, 1))
+    oc, cc = both_configs("raw", *margs)
+    so, sc = settings_pair(True, *cor)
+    go, gc = gas_pair(9.81)
+    g = capi.GpuSolver(capi.Mesh(cc), 4, "f64", gas=gc, settings=sc)
+    g.set_path(capi.PATH_STAGE)
+    g.init_case(capi.CASE_BAROCLINIC_JET)
+    q = g.get_state()
+    ne = q.shape[0]
+    assert ne == 786432 and float(np.abs(q[:, 1] / q[:, 0]).max()) > 25.0   # there is a jet
+    rng = np.random.default_rng(17)
+    q *= 1.0 + 1e-3 * np.sin(np.arange(ne, dtype=np.float64) * 0.37)[:, None, None]
+    q[:, 2:4] += 0.05 * rng.standard_normal((ne, 2, 1))
+    got = g.assemble_rhs(q)
+    omesh = port.mesh(oc)
+    o = omesh.solver(4, "f64", gas=go, settings=so)
+    faces, face_of = face_table(omesh), omesh.face_of
+    ranges = sample_ranges(ne, 5, 8, rng)
+    worst, n = check_samples(o, face_of, faces, q, got, ranges, TOL64)
+    print(f"channel-size parity: {n} sampled elements, scaled error {worst:.2e}")
