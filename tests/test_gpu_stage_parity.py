@@ -229,3 +229,24 @@ def test_channel_size_sampled_parity(port):
     ranges = sample_ranges(ne, 5, 8, rng)
     worst, n = check_samples(o, face_of, faces, q, got, ranges, TOL64)
     print(f"channel-size parity: {n} sampled elements, scaled error {worst:.2e}")
+
+
+def test_bench_size_partition_bitwise():
+    """Size-independent property at configs[1] itself (884,736 elements): the
+    state after one LSRK step on four Morton ranges (packed traces, interior /
+    boundary element groups, ghost faces evaluated by both sides) equals the
+    one-partition result bit for bit, on the stage path bench.py times
+    (tests/test_partition.cpp:94-114 at the bench size)."""
+    cfg = capi.bubble_mesh_config(5, False, base=(3, 3, 3))
+    states = []
+    for ranks in (1, 4):
+        g = capi.GpuSolver(capi.Mesh(cfg), 4, "f64", ranks=ranks)
+        g.set_path(capi.PATH_STAGE)
+        g.init_case(capi.CASE_BUBBLE_SHARP)
+        if ranks == 1:
+            dt = 0.5 * g.compute_dt(0.5)
+        g.step(dt)
+        states.append(g.get_state())
+        del g
+    assert np.isfinite(states[0]).all()
+    assert np.array_equal(states[0], states[1])
