@@ -250,3 +250,39 @@ def test_bench_size_partition_bitwise():
         del g
     assert np.isfinite(states[0]).all()
     assert np.array_equal(states[0], states[1])
+
+
+def test_bench_size_conservation_properties():
+    """Size-independent properties at the size of configs[1] (884,736
+    elements), evaluated by the device reductions (K6) on the k register of one
+    stage-path RHS of a rough state: mass and energy rates vanish; on the
+    periodic copy of the mesh with the dissipation off so does the entropy
+    production (test_kernels.cpp:164-183, 202-252; acceptance 1-2); on the mesh
+    as benched (walls) with the matrix dissipation on the production is
+    negative. (Dissipation on a mesh that is periodic in the direction of
+    gravity does not conserve energy, in the reference as here: phi jumps across
+    the wrap.)"""
+    prod = {}
+    for diss, periodic in ((0, True), (1, False)):
+        cfg = capi.bubble_mesh_config(5, periodic, base=(3, 3, 3))
+        g = capi.GpuSolver(capi.Mesh(cfg), 4, "f64", settings=capi.Settings(diss, 0, 0.0, 0.0, 0.0))
+        g.set_path(capi.PATH_STAGE)
+        g.init_case(capi.CASE_BUBBLE_SHARP)
+        q = g.get_state()
+        ne = q.shape[0]
+        rng = np.random.default_rng(3)
+        q *= 1.0 + 1e-3 * np.sin(np.arange(ne, dtype=np.float64) * 0.37)[:, None, None]
+        q[:, 1:4] += 0.5 * rng.standard_normal((ne, 3, 1))
+        g.set_state(q)
+        dt = g.compute_dt(0.5)
+        mass, energy, eta = g.quadrature_total(0), g.quadrature_total(4), g.total_entropy()
+        g.rhs(0.0, 1.0)
+        rates = g.quadrature_total(0, capi.REG_K), g.quadrature_total(4, capi.REG_K)
+        prod[diss] = g.entropy_production()
+        print(f"bench-size conservation (dissipation {diss}): mass drift per step {rates[0] * dt / mass:.2e}, "
+              f"energy {rates[1] * dt / energy:.2e}, entropy production {prod[diss]:.3e} (eta {eta:.3e})")
+        assert abs(rates[0]) * dt <= 1e-13 * abs(mass)
+        assert abs(rates[1]) * dt <= 1e-13 * abs(energy)
+        del g
+    assert abs(prod[0]) <= 1e-10 * abs(eta)
+    assert prod[1] < 0.0 and abs(prod[1]) > 1e3 * abs(prod[0])
