@@ -286,3 +286,29 @@ def test_bench_size_conservation_properties():
         del g
     assert abs(prod[0]) <= 1e-10 * abs(eta)
     assert prod[1] < 0.0 and abs(prod[1]) > 1e3 * abs(prod[0])
+
+
+def test_bench_size_step_stream_bitwise():
+    """The call bench.py's e2e figure times, at its size: two independent
+    states of configs[1] streamed through one solver (upload of the next and
+    download of the previous beside the step) equal set_state + step +
+    get_state per member, bit for bit."""
+    cfg = capi.bubble_mesh_config(5, False, base=(3, 3, 3))
+    g = capi.GpuSolver(capi.Mesh(cfg), 4, "f64")
+    g.set_path(capi.PATH_STAGE)
+    g.init_case(capi.CASE_BUBBLE_SHARP)
+    a = g.get_state()
+    b = a * (1.0 + 1e-3 * np.cos(np.arange(a.shape[0], dtype=np.float64) * 0.11))[:, None, None]
+    dt = 0.5 * g.compute_dt(0.5)
+    want = []
+    for q in (a, b):
+        g.set_state(q)
+        g.step(dt)
+        want.append(g.get_state())
+    out_a = np.empty_like(a)
+    g.set_state(a)
+    g.step_stream(dt, b, None)        # steps a, uploads b
+    g.step_stream(dt, None, out_a)    # steps b, downloads a's result
+    assert np.array_equal(out_a, want[0])
+    assert np.array_equal(g.get_state(), want[1])
+    assert not np.array_equal(want[0], want[1])
