@@ -146,14 +146,15 @@ def test_bench_size_sampled_parity(port):
 # the other points of the configs[1] order / precision sweep at the sizes
 # tools/sweep_probe.py and bench.py --order run them (~1e8 DOF each)
 SWEEP_POINTS = [(5, (5, 5, 5), 4, "f64"), (6, (1, 1, 1), 6, "f64"), (7, (15, 15, 15), 2, "f64"),
-                (4, (3, 3, 3), 5, "f32"), (7, (15, 15, 15), 2, "f32")]
+                (4, (3, 3, 3), 5, "f32"), (5, (5, 5, 5), 4, "f32"), (6, (1, 1, 1), 6, "f32"),
+                (7, (15, 15, 15), 2, "f32")]
 
 
 @pytest.mark.parametrize("order,base,refinement,prec", SWEEP_POINTS,
                          ids=[f"N{p[0]}-{p[3]}" for p in SWEEP_POINTS])
 def test_sweep_size_sampled_parity(port, order, base, refinement, prec):
     """The order / precision sweep of BASELINE.json configs[1] at its own sizes
-    (N = 5, 6, 7 in FP64, N = 4 and 7 in FP32; ~1e8 DOF each): one assemble_rhs
+    (N = 5, 6, 7 in FP64, N = 4 ... 7 in FP32; ~1e8 DOF each): one assemble_rhs
     on the stage path, the oracle on ~190 sampled elements (first / last element
     group, evenly spaced group boundaries, random places), as
     test_bench_size_sampled_parity does for N = 4 FP64."""
