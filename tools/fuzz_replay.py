@@ -20,7 +20,7 @@ for trial in range(target + 1):
     periodic = bool(rng.integers(0, 2))
     ranks = int(rng.integers(1, 5))
     diss = bool(rng.integers(0, 2))
-    path = [capi.PATH_SPLIT, capi.PATH_FUSED][int(rng.integers(0, 2))]
+    path = [capi.PATH_SPLIT, capi.PATH_FUSED, capi.PATH_STAGE][int(rng.integers(0, 3))]
     level = 1 if order > 4 else int(rng.integers(1, 3))
     case_seed = int(rng.integers(1, 1 << 30))
     a_old = 0.0 if rng.random() < 0.3 else float(rng.uniform(-1.5, 1.5))
@@ -47,4 +47,7 @@ for trial in range(target + 1):
                 got = g.assemble_rhs(q, out0.copy(), a_old, an)
                 errs = [float(np.abs(got[:, v].astype(np.float64) - want[:, v]).max()) / ((abs(an) + abs(a_old)) * scale[v])
                         for v in range(5)]
-                print(f"  ranks={r} path={p} a_new={an:.4f}: scaled error per variable " + " ".join(f"{e:.2e}" for e in errs))
+                v = int(np.argmax(errs))
+                e_at, n_at = np.unravel_index(int(np.abs(got[:, v].astype(np.float64) - want[:, v]).argmax()), got[:, v].shape)
+                print(f"  ranks={r} path={p} a_new={an:.4f}: scaled error per variable " + " ".join(f"{e:.2e}" for e in errs)
+                      + f" | worst at element {e_at}, node {n_at}, variable {v}")
